@@ -1,0 +1,106 @@
+// ref_batch.cpp -- batch-over-records driver around the UNMODIFIED reference core.
+//
+// TEST INFRASTRUCTURE ONLY (checker + CPU baseline).  Linked by oracle/Makefile
+// with /root/reference/proj/src/{mat3,invariants,eigensolver}.cpp compiled in
+// place with the reference's own flags (-std=c++20 -O3 -ffp-contract=off,
+// proj/src/CMakeLists.txt:5-10) into oracle/_ref/libeig33_ref.so.  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+// load it.  It calls the reference's public per-matrix API:
+//   eig33::invariants(const Mat3&, AlgorithmVariant)  include/eig33/invariants.hpp:74
+//   eig33::eigvals(const Mat3&)                       include/eig33/eigensolver.hpp:39
+//   eig33::eigvalss(const Mat3&)                      include/eig33/eigensolver.hpp:45
+//   eig33::triple_angle(double, double)               include/eig33/eigensolver.hpp:21
+//   eig33::eigvals_checksum_loop(const Mat3&, n)      include/eig33/eigensolver.hpp:57
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "eig33/eigensolver.hpp"
+#include "eig33/invariants.hpp"
+#include "eig33/mat3.hpp"
+
+namespace {
+
+eig33::Mat3 load(const double* p) {
+  eig33::Mat3 m;
+  std::memcpy(m.e.data(), p, sizeof(double) * 9);
+  return m;
+}
+
+template <class F>
+void parallel_shards(std::size_t n, int nthreads, F&& body) {
+  if (nthreads <= 1 || n < 2) {
+    body(std::size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nthreads);
+  for (int t = 0; t < nthreads; ++t) {
+    const std::size_t lo = n * t / nthreads, hi = n * (t + 1) / nthreads;
+    pool.emplace_back([&body, lo, hi] { body(lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+// n x {i1, j2, j3, disc}
+int ref_invariants(const double* a, std::size_t n, double* inv, int nthreads) {
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto s = eig33::invariants(load(a + 9 * i), eig33::AlgorithmVariant::Stable);
+      inv[4 * i + 0] = s.i1;
+      inv[4 * i + 1] = s.j2;
+      inv[4 * i + 2] = s.j3;
+      inv[4 * i + 3] = s.disc;
+    }
+  });
+  return 0;
+}
+
+// n x {l1, l2, l3}; adv nullable (n bytes)
+int ref_eigvals(const double* a, std::size_t n, double* lam, std::uint8_t* adv, int nthreads) {
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto t = eig33::eigvals(load(a + 9 * i));
+      lam[3 * i + 0] = t.lambda1;
+      lam[3 * i + 1] = t.lambda2;
+      lam[3 * i + 2] = t.lambda3;
+      if (adv) adv[i] = t.non_real_advisory ? 1 : 0;
+    }
+  });
+  return 0;
+}
+
+// status[i] = 1 where eigvalss throws NotSymmetric (lambda = NaN there)
+int ref_eigvalss(const double* a, std::size_t n, double* lam, std::uint8_t* status, int nthreads) {
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      try {
+        const auto t = eig33::eigvalss(load(a + 9 * i));
+        lam[3 * i + 0] = t.lambda1;
+        lam[3 * i + 1] = t.lambda2;
+        lam[3 * i + 2] = t.lambda3;
+        if (status) status[i] = 0;
+      } catch (const eig33::NotSymmetric&) {
+        lam[3 * i + 0] = lam[3 * i + 1] = lam[3 * i + 2] = __builtin_nan("");
+        if (status) status[i] = 1;
+      }
+    }
+  });
+  return 0;
+}
+
+int ref_triple_angle(const double* j3, const double* disc, std::size_t n, double* phi) {
+  for (std::size_t i = 0; i < n; ++i) phi[i] = eig33::triple_angle(j3[i], disc[i]).phi;
+  return 0;
+}
+
+std::uint64_t ref_checksum_loop(const double* a, std::uint64_t n) {
+  return eig33::eigvals_checksum_loop(load(a), n);
+}
+
+}  // extern "C"

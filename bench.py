@@ -1,0 +1,406 @@
+"""Throughput benchmark of the batched eig33 hot path (BASELINE.json metric:
+3x3 fp64 eigvals/sec at 1/2/4/8 B200; % of HBM/FP64 roofline).
+
+A step = one pass of the fused invariants -> eigenvalues kernel over one batch
+of BASELINE config 3 (general nonsymmetric A = V diag(l) V^-1, V Gaussian with
+cond2(V) <= 1e3, l ~ U[-10,10]), 2^28 records per GPU (19.3 GB in, 6.4 GB out),
+lambda-only output.  Weak scaling: rank r processes records
+[r*2^28, (r+1)*2^28) of one global counter-based corpus, no collective on the
+data path (torch.distributed is used only for the barrier and the max-over-ranks
+timing reduction).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line on rank 0.  --impl reference times the reference's own
+CPU implementation (oracle/_ref: the unmodified reference core compiled from
+/root/reference/proj/src; else the oracle port) on this box's host cores.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "3×3 fp64 eigvals/sec at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "matrices/s"
+N_PER_GPU_DEFAULT = 1 << 28
+SEED = 0x2511_00292
+BYTES_PER_REC = 96          # 72 B in + 24 B lambda out
+FP64_OPS_PER_REC = 357      # frozen algorithmic FP64-pipe count
+HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=N_PER_GPU_DEFAULT, help="records per GPU")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# host-side corpus for the reference arm (same recipe as eig33_gen.cu config 3)
+# ---------------------------------------------------------------------------
+def config3_numpy(n, seed):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, 9))
+    filled = 0
+    while filled < n:
+        m = int((n - filled) * 1.3) + 16
+        v = rng.standard_normal((m, 3, 3))
+        s = np.linalg.svd(v, compute_uv=False)
+        v = v[s[:, 0] / s[:, 2] <= 1e3]
+        lam = rng.uniform(-10, 10, (v.shape[0], 3))
+        # (V*D)*inverse_adjugate(V), reference association (bench.cpp:69-75)
+        vd = v * lam[:, None, :]
+        cof = np.empty_like(v)
+        cof[:, 0, 0] = v[:, 1, 1] * v[:, 2, 2] - v[:, 1, 2] * v[:, 2, 1]
+        cof[:, 0, 1] = v[:, 1, 2] * v[:, 2, 0] - v[:, 1, 0] * v[:, 2, 2]
+        cof[:, 0, 2] = v[:, 1, 0] * v[:, 2, 1] - v[:, 1, 1] * v[:, 2, 0]
+        cof[:, 1, 0] = v[:, 0, 2] * v[:, 2, 1] - v[:, 0, 1] * v[:, 2, 2]
+        cof[:, 1, 1] = v[:, 0, 0] * v[:, 2, 2] - v[:, 0, 2] * v[:, 2, 0]
+        cof[:, 1, 2] = v[:, 0, 1] * v[:, 2, 0] - v[:, 0, 0] * v[:, 2, 1]
+        cof[:, 2, 0] = v[:, 0, 1] * v[:, 1, 2] - v[:, 0, 2] * v[:, 1, 1]
+        cof[:, 2, 1] = v[:, 0, 2] * v[:, 1, 0] - v[:, 0, 0] * v[:, 1, 2]
+        cof[:, 2, 2] = v[:, 0, 0] * v[:, 1, 1] - v[:, 0, 1] * v[:, 1, 0]
+        det = (v[:, 0, 0] * cof[:, 0, 0] + v[:, 0, 1] * cof[:, 0, 1]) + v[:, 0, 2] * cof[:, 0, 2]
+        vinv = np.transpose(cof, (0, 2, 1)) / det[:, None, None]
+        a = np.einsum("nij,njk->nik", vd, vinv)
+        take = min(a.shape[0], n - filled)
+        out[filled:filled + take] = a[:take].reshape(take, 9)
+        filled += take
+    return np.ascontiguousarray(out)
+
+
+def cpu_lib():
+    """(ctypes lib, kind): the compiled reference core if built, else the port."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "libeig33_ref.so")
+    if os.path.exists(ref):
+        return ctypes.CDLL(ref), "reference"
+    port = os.path.join(ROOT, "oracle", "liboracle.so")
+    if not os.path.exists(port):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
+    return ctypes.CDLL(port), "port"
+
+
+def cpu_eigvals_rate(a, seconds, threads):
+    """Stream eigvals over the host sample `a` repeatedly for ~`seconds`;
+    returns (matrices/s, passes)."""
+    import numpy as np
+
+    L, kind = cpu_lib()
+    n = a.shape[0]
+    lam = np.empty((n, 3))
+    pa, pl = a.ctypes.data_as(ctypes.c_void_p), lam.ctypes.data_as(ctypes.c_void_p)
+
+    def one():
+        if kind == "reference":
+            L.ref_eigvals(pa, ctypes.c_size_t(n), pl, None, threads)
+        else:
+            L.orc_eigvals_mt(pa, ctypes.c_size_t(n), None, pl, threads)
+
+    one()  # warm-up pass
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        one()
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return n * passes / el, passes, kind
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of k_fused from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k_fused.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("records_per_launch")
+    except (OSError, ValueError):
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    sample = 1 << 22
+    a = config3_numpy(sample, SEED)
+    L, kind = cpu_lib()
+    lam = np.empty((sample, 3))
+    pa, pl = a.ctypes.data_as(ctypes.c_void_p), lam.ctypes.data_as(ctypes.c_void_p)
+
+    def step():
+        if kind == "reference":
+            L.ref_eigvals(pa, ctypes.c_size_t(sample), pl, None, threads)
+        else:
+            L.orc_eigvals_mt(pa, ctypes.c_size_t(sample), None, pl, threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    v = sample * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "config3 general nonsymmetric, cond2(V)<=1e3, lambda~U[-10,10]",
+                   "records_per_step": sample, "outputs": "lambda only"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample} config-3 records per step (numpy-generated, seed {SEED}), "
+                                   f"eig33::eigvals streamed over contiguous shards on {threads} threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2511_00292_b200 as eig
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    L = eig.lib()
+    n = args.n
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        a = eig.generate(3, n, seed=SEED, first_index=rank * n, device=dev)
+        lam = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    stream.synchronize()
+    pa, pl = ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(lam.data_ptr())
+    st = ctypes.c_void_p(stream.cuda_stream)
+
+    def step():
+        rc = L.eig33cu_eigvals(pa, n, None, pl, None, st)
+        if rc:
+            raise RuntimeError(L.eig33cu_last_error().decode())
+
+    # FP64 issue-rate peak on this GPU (roofline denominator), before the run
+    L.eig33_probe_fp64_rate.restype = ctypes.c_double
+    L.eig33_probe_fp64_rate.argtypes = [ctypes.c_int]
+    fp64_rate = L.eig33_probe_fp64_rate(20)
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    total = n * world
+    value = total * args.steps / (ms_max * 1e-3)
+
+    # ---- e2e through the public host-buffer API (pinned host in/out) ----
+    e2e = None
+    if not args.no_e2e:
+        h_a = torch.empty((n, 9), dtype=torch.float64, pin_memory=True)
+        h_a.copy_(a)
+        h_l = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+        pha, phl = ctypes.c_void_p(h_a.data_ptr()), ctypes.c_void_p(h_l.data_ptr())
+        rc = L.eig33_eigvals_host(pha, n, None, phl, None, local_rank)  # warm (staging alloc)
+        if rc:
+            raise RuntimeError(L.eig33cu_last_error().decode())
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            L.eig33_eigvals_host(pha, n, None, phl, None, local_rank)
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        same = bool(torch.equal(h_l.view(torch.int64), lam.cpu().view(torch.int64)))
+        e2e = {"value": total * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": n * 72,
+               "d2h_bytes_per_step": n * 24, "steps": args.e2e_steps,
+               "api": "eig33_eigvals_host (pinned host buffers, chunked H2D/kernel/D2H over 3 streams)",
+               "bitwise_equal_to_device_path": same}
+        del h_a, h_l
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline ----
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs") or HBM_PEAK_FALLBACK
+    per_launch_s = ms_step * 1e-3
+    hbm_ach = n * BYTES_PER_REC / per_launch_s / 1e9
+    fp64_ach = n * FP64_OPS_PER_REC / per_launch_s / 1e12
+    fp64_peak = fp64_rate / 1e12 if fp64_rate > 0 else None
+    traffic, recs = ncu_traffic()
+    traffic_per_launch = traffic * n / recs if traffic and recs else None
+    hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
+           "frac": hbm_ach / hbm_peak,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks.get("hbm_gbs") else "fallback"}
+    fp64 = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "T fp64-inst/s",
+            "frac": fp64_ach / fp64_peak if fp64_peak else None,
+            "peak_source": "measured on this GPU: DFMA issue rate (eig33_probe_fp64_rate)",
+            "ops_per_record": FP64_OPS_PER_REC}
+    # the binding roof is the slower one (BASELINE north_star): the one with the higher frac
+    binding = fp64 if (fp64["frac"] or 0) >= hbm["frac"] else hbm
+    roofline = dict(binding)
+    roofline["traffic"] = traffic_per_launch
+    roofline["algorithmic_bytes_per_launch"] = n * BYTES_PER_REC
+    roofline["kernel"] = "k_fused<eigvals,TMA> (1 launch per step)"
+    roofline["both"] = {"hbm": hbm, "fp64": fp64}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        samp = 1 << 22
+        a_host = a[:samp].cpu().numpy()
+        threads = os.cpu_count() or 1
+        rate, passes, kind = cpu_eigvals_rate(a_host, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"first {samp} records of this run's config-3 batch, {passes} timed passes "
+                         f"(~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "BASELINE config 3 (configs[2]): general nonsymmetric A=(V diag(l))V^-1, "
+                               "V~N(0,1) with cond2(V)<=1e3, l~U[-10,10]; lambda-only output",
+                   "records_per_gpu": n, "parallelism": f"dp{world} (contiguous shards, no collective)",
+                   "seed": SEED, "l2": "inputs larger than L2 (19.3 GB per GPU per step)"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk,
+        "fp64_probe_inst_per_s": fp64_rate,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

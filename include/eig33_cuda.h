@@ -1,0 +1,95 @@
+/*
+ * eig33_cuda.h -- C ABI of the B200 (sm_100a) batched eig33 hot path.
+ *
+ * Drop-in boundary for the reference's per-matrix C++ API
+ * (/root/reference/proj/include/eig33/*.hpp), lifted to contiguous batches of
+ * the same 72-byte row-major fp64 record (Mat3, include/eig33/mat3.hpp:24-28).
+ * Plain pointers and sizes only; no exceptions cross it; every call returns a
+ * status code:
+ *   EIG33_OK (0), EIG33_ECUDA (1), EIG33_EINVAL (2), EIG33_ENOTSYM (3).
+ * eig33cu_last_error() describes the last non-zero status of the calling thread.
+ *
+ * Device-pointer entry points (eig33cu_*) are stream-ordered and asynchronous
+ * with respect to the host; `stream` is a cudaStream_t (NULL = legacy default
+ * stream).  Host-pointer entry points (eig33_*_host, eig33_multi_*) are
+ * synchronous and move data through pinned staging themselves.
+ *
+ * Packed output layouts (what the benchmark measures):
+ *   inv   : n x 4 doubles {i1, j2, j3, disc}        (InvariantSet minus variant)
+ *   lam   : n x 3 doubles {l1 <= l2 <= l3}          (EigenTriple minus the flag)
+ *   flags : n bytes, bit0 = non_real_advisory, bit1 = not_symmetric (eigvalss)
+ * Any of inv / flags may be NULL to skip that output.
+ */
+#ifndef EIG33_CUDA_H_
+#define EIG33_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIG33_OK 0
+#define EIG33_ECUDA 1
+#define EIG33_EINVAL 2
+#define EIG33_ENOTSYM 3
+
+#define EIG33_FLAG_ADVISORY 0x1u
+#define EIG33_FLAG_NOT_SYMMETRIC 0x2u
+
+/* ABI version, (major << 16) | minor. */
+int eig33cu_version(void);
+/* Thread-local description of the last failure ("" if none). */
+const char* eig33cu_last_error(void);
+
+/* Batched eig33::invariants(a, AlgorithmVariant::Stable)
+ * (reference include/eig33/invariants.hpp:74, src/invariants.cpp:76-85).
+ * Bit-exact.  d_a: n x 9 doubles, d_inv: n x 4 doubles. */
+int eig33cu_invariants(const double* d_a, size_t n, double* d_inv, void* stream);
+
+/* Batched eig33::eigvals (reference include/eig33/eigensolver.hpp:39,
+ * src/eigensolver.cpp:91-95), fused with the invariants: they never
+ * round-trip through HBM unless d_inv is non-NULL.  d_flags (optional)
+ * receives non_real_advisory in bit0 (bit-exact vs src/eigensolver.cpp:54). */
+int eig33cu_eigvals(const double* d_a, size_t n, double* d_inv, double* d_lam,
+                    uint8_t* d_flags, void* stream);
+
+/* Batched eig33::eigvalss (reference include/eig33/eigensolver.hpp:45,
+ * src/eigensolver.cpp:97-117).  A matrix failing the symmetry gate (where the
+ * scalar API throws NotSymmetric) gets NaN outputs and bit1 in d_flags. */
+int eig33cu_eigvalss(const double* d_a, size_t n, double* d_inv, double* d_lam,
+                     uint8_t* d_flags, void* stream);
+
+/* Batched eig33::triple_angle (reference include/eig33/eigensolver.hpp:21,
+ * src/eigensolver.cpp:84-89): phi[i] = atan2(sqrt(27*max(disc,0)), 27*j3). */
+int eig33cu_triple_angle(const double* d_j3, const double* d_disc, size_t n, double* d_phi,
+                         void* stream);
+
+/* Synchronous host-buffer versions on one device (chunked, pipelined
+ * H2D / kernel / D2H over 3 streams).  eig33_eigvalss_host returns
+ * EIG33_ENOTSYM if any matrix failed the symmetry gate (outputs still written). */
+int eig33_invariants_host(const double* h_a, size_t n, double* h_inv, int device);
+int eig33_eigvals_host(const double* h_a, size_t n, double* h_inv, double* h_lam,
+                       uint8_t* h_flags, int device);
+int eig33_eigvalss_host(const double* h_a, size_t n, double* h_inv, double* h_lam,
+                        uint8_t* h_flags, int device);
+
+/* Multi-GPU host driver: contiguous even-aligned shards
+ * [2*floor(g*n/(2G)), 2*floor((g+1)*n/(2G))) on devices 0..ngpu-1, one host
+ * thread and stream set per device, no inter-GPU communication.  Results are
+ * bitwise identical for every ngpu. */
+int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_lam,
+                        uint8_t* h_flags, int ngpu);
+
+/* Synthetic corpora of the benchmark configs (BASELINE.json configs[0..4]),
+ * counter-based: record i depends only on (config, seed, first_index + i), so
+ * any shard regenerates independently.  config in 1..5. */
+int eig33cu_generate(int config, uint64_t seed, uint64_t first_index, size_t n, double* d_a,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EIG33_CUDA_H_ */

@@ -1,0 +1,266 @@
+"""Batched B200 (sm_100a) evaluation of the eig33 hot path (arXiv 2511.00292).
+
+Python mirror of the reference's public API (reference proj/python/eig33 and
+proj/bindings/module.cpp:79-99: ``eigvals``, ``eigvalss``, ``invariants``,
+``triple_angle``), lifted from one matrix to a contiguous batch of the same
+72-byte row-major fp64 record.  Every call goes through the C ABI of
+``_eig33cuda.so`` (include/eig33_cuda.h); there is no CPU fallback -- a missing
+extension or a missing GPU raises.
+
+Inputs are float64 arrays of shape (n, 3, 3) or (n, 9):
+  * torch CUDA tensors -> computed in place on that device, on the current
+    torch stream (device-pointer entry points, stream-ordered);
+  * numpy arrays / CPU tensors -> host-buffer entry points (pinned, chunked
+    H2D / kernel / D2H pipeline), results returned as numpy arrays.
+
+Error behaviour follows the reference bindings: malformed shapes raise
+ValueError (module.cpp:16-39 ``to_mat``), ``eigvalss`` on a matrix that fails
+the symmetry gate raises ValueError (module.cpp turns NotSymmetric into
+ValueError), CUDA failures raise RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "eigvals", "eigvalss", "invariants", "triple_angle", "generate", "multi_eigvals",
+    "lib", "EigResult", "eps_mach", "FLAG_ADVISORY", "FLAG_NOT_SYMMETRIC",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_eig33cuda.so")
+
+eps_mach = 2.0 ** -53  # reference include/eig33/mat3.hpp:10
+FLAG_ADVISORY = 0x1
+FLAG_NOT_SYMMETRIC = 0x2
+EIG33_OK, EIG33_ECUDA, EIG33_EINVAL, EIG33_ENOTSYM = 0, 1, 2, 3
+
+# Every symbol include/eig33_cuda.h declares (checked by tests/test_capi.py).
+C_ABI_SYMBOLS = (
+    "eig33cu_version", "eig33cu_last_error", "eig33cu_invariants", "eig33cu_eigvals",
+    "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
+    "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
+)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree extension (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise ImportError(
+            f"{_SO} is missing: build it with `python -m paper_2511_00292_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(_SO)
+    P, S, I, U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+    sig = {
+        "eig33cu_version": ([], I),
+        "eig33cu_last_error": ([], ctypes.c_char_p),
+        "eig33cu_invariants": ([P, S, P, P], I),
+        "eig33cu_eigvals": ([P, S, P, P, P, P], I),
+        "eig33cu_eigvalss": ([P, S, P, P, P, P], I),
+        "eig33cu_triple_angle": ([P, P, S, P, P], I),
+        "eig33_invariants_host": ([P, S, P, I], I),
+        "eig33_eigvals_host": ([P, S, P, P, P, I], I),
+        "eig33_eigvalss_host": ([P, S, P, P, P, I], I),
+        "eig33_multi_eigvals": ([P, S, P, P, P, I], I),
+        "eig33cu_generate": ([I, U64, U64, S, P, P], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str):
+    if rc == EIG33_OK:
+        return
+    msg = lib().eig33cu_last_error().decode(errors="replace")
+    if rc == EIG33_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    if rc == EIG33_ENOTSYM:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+
+def _torch():
+    import torch  # local: numpy-only users need not import torch
+
+    return torch
+
+
+def _is_cuda_tensor(a) -> bool:
+    try:
+        torch = _torch()
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def _records_np(a) -> np.ndarray:
+    if hasattr(a, "detach") and hasattr(a, "numpy"):
+        a = a.detach().cpu().numpy()
+    arr = np.asarray(a)
+    if arr.dtype != np.float64:
+        if not np.issubdtype(arr.dtype, np.number):
+            raise ValueError("matrix entries must be numeric")
+        arr = arr.astype(np.float64)
+    if arr.ndim == 2 and arr.shape == (3, 3):
+        arr = arr.reshape(1, 9)
+    elif arr.ndim == 3 and arr.shape[1:] == (3, 3):
+        arr = arr.reshape(arr.shape[0], 9)
+    elif arr.ndim == 2 and arr.shape[1] == 9:
+        pass
+    elif arr.ndim == 1 and arr.shape[0] == 9:
+        arr = arr.reshape(1, 9)
+    else:
+        raise ValueError(f"expected (n,3,3) or (n,9) matrices, got shape {arr.shape}")
+    return np.ascontiguousarray(arr)
+
+
+def _records_cuda(a):
+    torch = _torch()
+    if a.dtype != torch.float64:
+        raise ValueError("CUDA input must be float64")
+    if a.dim() == 3 and tuple(a.shape[1:]) == (3, 3):
+        a = a.reshape(a.shape[0], 9)
+    elif a.dim() == 2 and a.shape[1] == 9:
+        pass
+    elif a.dim() == 2 and tuple(a.shape) == (3, 3):
+        a = a.reshape(1, 9)
+    else:
+        raise ValueError(f"expected (n,3,3) or (n,9) matrices, got shape {tuple(a.shape)}")
+    return a.contiguous()
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream(a):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+
+
+class EigResult(tuple):
+    """(lam, inv, flags) with attribute access; inv / flags may be None."""
+
+    def __new__(cls, lam, inv=None, flags=None):
+        obj = super().__new__(cls, (lam, inv, flags))
+        return obj
+
+    lam = property(lambda s: s[0])
+    inv = property(lambda s: s[1])
+    flags = property(lambda s: s[2])
+
+    @property
+    def non_real_advisory(self):
+        f = self[2]
+        return None if f is None else (f & FLAG_ADVISORY) != 0
+
+
+def _eig_common(entry_dev, entry_host, what, a, want_inv, want_flags, device):
+    L = lib()
+    if _is_cuda_tensor(a):
+        torch = _torch()
+        a = _records_cuda(a)
+        n = a.shape[0]
+        with torch.cuda.device(a.device):
+            lam = torch.empty((n, 3), dtype=torch.float64, device=a.device)
+            inv = torch.empty((n, 4), dtype=torch.float64, device=a.device) if want_inv else None
+            flags = torch.empty((n,), dtype=torch.uint8, device=a.device) if want_flags else None
+            _check(getattr(L, entry_dev)(_ptr(a), n, _ptr(inv), _ptr(lam), _ptr(flags), _stream(a)),
+                   what)
+        return EigResult(lam, inv, flags)
+    arr = _records_np(a)
+    n = arr.shape[0]
+    lam = np.empty((n, 3))
+    inv = np.empty((n, 4)) if want_inv else None
+    flags = np.empty((n,), np.uint8) if want_flags else None
+    _check(getattr(L, entry_host)(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(device)), what)
+    return EigResult(lam, inv, flags)
+
+
+def eigvals(a, *, return_invariants=False, return_flags=False, device=0) -> EigResult:
+    """Batched ``eig33::eigvals`` (reference include/eig33/eigensolver.hpp:39).
+
+    Returns EigResult(lam (n,3) ascending, inv (n,4) {i1,j2,j3,disc} or None,
+    flags (n,) uint8 with bit0 = non_real_advisory, or None)."""
+    return _eig_common("eig33cu_eigvals", "eig33_eigvals_host", "eigvals", a, return_invariants,
+                       return_flags, device)
+
+
+def eigvalss(a, *, return_invariants=False, return_flags=False, device=0) -> EigResult:
+    """Batched ``eig33::eigvalss`` (reference include/eig33/eigensolver.hpp:45).
+
+    Host inputs: raises ValueError if any matrix fails the symmetry gate, like
+    the reference binding.  CUDA inputs are stream-ordered, so failures are
+    reported per matrix in flags bit1 (and NaN outputs) instead of raising."""
+    return _eig_common("eig33cu_eigvalss", "eig33_eigvalss_host", "eigvalss", a,
+                       return_invariants, return_flags, device)
+
+
+def invariants(a, *, device=0):
+    """Batched ``eig33::invariants(a, AlgorithmVariant::Stable)``: (n,4) {i1,j2,j3,disc}."""
+    L = lib()
+    if _is_cuda_tensor(a):
+        torch = _torch()
+        a = _records_cuda(a)
+        with torch.cuda.device(a.device):
+            inv = torch.empty((a.shape[0], 4), dtype=torch.float64, device=a.device)
+            _check(L.eig33cu_invariants(_ptr(a), a.shape[0], _ptr(inv), _stream(a)), "invariants")
+        return inv
+    arr = _records_np(a)
+    inv = np.empty((arr.shape[0], 4))
+    _check(L.eig33_invariants_host(_ptr(arr), arr.shape[0], _ptr(inv), int(device)), "invariants")
+    return inv
+
+
+def triple_angle(j3, disc):
+    """Batched ``eig33::triple_angle`` on CUDA float64 vectors (eigensolver.hpp:21)."""
+    torch = _torch()
+    if not (_is_cuda_tensor(j3) and _is_cuda_tensor(disc)):
+        raise ValueError("triple_angle takes CUDA float64 tensors")
+    j3 = j3.reshape(-1).contiguous()
+    disc = disc.reshape(-1).contiguous()
+    if j3.shape != disc.shape or j3.dtype != torch.float64 or disc.dtype != torch.float64:
+        raise ValueError("j3 and disc must be float64 tensors of equal length")
+    phi = torch.empty_like(j3)
+    with torch.cuda.device(j3.device):
+        _check(lib().eig33cu_triple_angle(_ptr(j3), _ptr(disc), j3.numel(), _ptr(phi), _stream(j3)),
+               "triple_angle")
+    return phi
+
+
+def generate(config: int, n: int, seed: int = 0, first_index: int = 0, device="cuda"):
+    """Synthetic corpus of BASELINE config 1..5 as an (n,9) CUDA float64 tensor."""
+    torch = _torch()
+    out = torch.empty((n, 9), dtype=torch.float64, device=device)
+    with torch.cuda.device(out.device):
+        _check(lib().eig33cu_generate(int(config), int(seed) & (2**64 - 1), int(first_index), int(n),
+                                      _ptr(out), _stream(out)), "generate")
+    return out
+
+
+def multi_eigvals(a, ngpu: int, *, return_invariants=False, return_flags=False) -> EigResult:
+    """Host batch sharded over devices 0..ngpu-1 (eig33_multi_eigvals)."""
+    arr = _records_np(a)
+    n = arr.shape[0]
+    lam = np.empty((n, 3))
+    inv = np.empty((n, 4)) if return_invariants else None
+    flags = np.empty((n,), np.uint8) if return_flags else None
+    _check(lib().eig33_multi_eigvals(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(ngpu)),
+           "multi_eigvals")
+    return EigResult(lam, inv, flags)

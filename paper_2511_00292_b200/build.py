@@ -1,0 +1,107 @@
+"""Build recipe for the in-tree native artefacts (no torch JIT cache involved).
+
+  paper_2511_00292_b200/_eig33cuda.so   product: sm_100a kernels + C ABI (nvcc)
+  oracle/liboracle.so                   checker: C restatement (gcc)
+  oracle/_ref/libeig33_ref.so           checker: compiled reference core (only
+                                        when /root/reference is present)
+  tests/hostmath/libhostmath.so         test harness: product math built for CPU
+
+Usage: python -m paper_2511_00292_b200.build [--product-only]
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "_eig33cuda.so")
+REF = "/root/reference/proj"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo",
+    "--fmad=false",          # bit-exact invariants: no contraction (reference proj/src/CMakeLists.txt:9-10)
+    "-std=c++17",
+    "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
+    "-Xptxas", "-v",
+]
+SOURCES = ["eig33_kernels.cu", "eig33_gen.cu", "eig33_host.cpp", "eig33_probe.cu"]
+
+
+def _nvcc():
+    for c in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _run(cmd, log=None):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if log is not None:
+        with open(log, "w") as f:
+            f.write(" ".join(cmd) + "\n" + r.stdout)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout)
+        raise RuntimeError("command failed: " + " ".join(cmd[:3]) + " ...")
+    return r.stdout
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_product(force=False):
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [
+        os.path.join(CSRC, h) for h in ("eig33_math.cuh", "eig33_tables.h", "eig33_internal.h")
+    ] + [os.path.join(ROOT, "include", "eig33_cuda.h")]
+    if not force and not _stale(SO, deps):
+        return SO
+    objs = []
+    build_dir = os.path.join(HERE, "build")
+    os.makedirs(build_dir, exist_ok=True)
+    nvcc = _nvcc()
+    for s in SOURCES:
+        o = os.path.join(build_dir, s + ".o")
+        _run([nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o],
+             log=os.path.join(build_dir, s + ".log"))
+        objs.append(o)
+    tmp = SO + ".tmp"
+    _run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
+          "-Xcompiler", "-pthread"])
+    os.replace(tmp, SO)
+    return SO
+
+
+def build_oracle():
+    make = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"]
+    _run(make)
+    if os.path.isdir(REF):
+        _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref", "REF=" + REF])
+
+
+def build_hostmath():
+    src = os.path.join(ROOT, "tests", "hostmath", "hostmath.cpp")
+    out = os.path.join(ROOT, "tests", "hostmath", "libhostmath.so")
+    deps = [src, os.path.join(CSRC, "eig33_math.cuh"), os.path.join(CSRC, "eig33_tables.h")]
+    if _stale(out, deps):
+        _run(["g++", "-O2", "-mfma", "-ffp-contract=off", "-fPIC", "-shared", "-std=c++17",
+              "-o", out, src, "-lm"])
+
+
+def build_all(force=False):
+    build_product(force)
+    build_oracle()
+    build_hostmath()
+
+
+if __name__ == "__main__":
+    if "--product-only" in sys.argv:
+        print(build_product(force="--force" in sys.argv))
+    else:
+        build_all(force="--force" in sys.argv)
+        print("built", SO)

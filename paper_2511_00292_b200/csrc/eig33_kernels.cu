@@ -1,0 +1,390 @@
+// eig33_kernels.cu -- sm_100a kernels and device-pointer C ABI of the batched
+// eig33 hot path (see include/eig33_cuda.h and DESIGN.md).
+//
+// MUST be compiled with --fmad=false: the invariant arithmetic is bit-exact
+// against the reference only without contraction (proj/src/CMakeLists.txt:9-10).
+//
+// Kernel map
+//   k_fused<MODE, TMA>   one persistent kernel for eigvals / invariants /
+//                        eigvalss: 256 records per tile, one record per thread.
+//                        Input tiles (256 x 72 B = 18 KB) stream HBM -> SMEM
+//                        through cp.async.bulk (TMA 1D) into a STAGES-deep ring
+//                        completed on mbarriers; each thread reads its record
+//                        from SMEM (72-B stride: conflict-free per half-warp),
+//                        computes invariants -> eigenvalues in registers, and
+//                        the tile's outputs are staged in SMEM so the HBM
+//                        stores are contiguous 8-B-per-lane runs.
+//   k_advisory           deferred non_real_advisory: block-compacts the records
+//                        that k_fused marked pending (disc < 0) and evaluates
+//                        disc_tolerance only for them (bit-exact).
+//   k_triple_angle       batched triple_angle.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#define EIG33_TABLE_DECL static __constant__
+#include "eig33_tables.h"
+#include "eig33_math.cuh"
+#include "eig33_internal.h"
+#include "../../include/eig33_cuda.h"
+
+namespace eig33b {
+
+constexpr int kThreads = 256;  // records per tile == threads per block
+constexpr int kStages = 2;     // TMA ring depth
+constexpr int kTabDoubles = EIG33_AT_N + 4 * EIG33_AT_N * 2 + EIG33_SC_N * 5;  // 243
+constexpr uint32_t kTileBytes = kThreads * 9 * sizeof(double);                 // 18432
+constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
+
+enum Mode { kEig = 0, kInv = 1, kSym = 2 };
+
+struct __align__(16) Smem {
+  double in[kStages][kThreads * 9];
+  double lam[kThreads * 3];
+  double inv[kThreads * 4];
+  double tab[kTabDoubles + 1];
+  unsigned long long bar[kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
+__device__ __forceinline__ void load_tables(double* tab) {
+  for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) {
+    double v;
+    if (i < EIG33_AT_N)
+      v = eig33_at_c[i];
+    else if (i < EIG33_AT_N + 8 * EIG33_AT_N)
+      v = eig33_at_t[i - EIG33_AT_N];
+    else
+      v = eig33_sc[i - 9 * EIG33_AT_N];
+    tab[i] = v;
+  }
+}
+
+// Persistent fused kernel.  One tile = kThreads consecutive records.
+template <int MODE, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
+            double* __restrict__ lam, uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int t = threadIdx.x;
+  const long long ntiles = (n + kThreads - 1) / kThreads;
+  const long long full_tiles = n / kThreads;
+
+  if (TMA && t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  load_tables(S.tab);
+  __syncthreads();
+  const double* at_c = S.tab;
+  const double* at_t = S.tab + EIG33_AT_N;
+  const double* sc = S.tab + 9 * EIG33_AT_N;
+
+  if (TMA && t == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const long long tile = blockIdx.x + (long long)s * gridDim.x;
+      if (tile < full_tiles) {
+        mbar_expect_tx(&S.bar[s], kTileBytes);
+        bulk_load(S.in[s], a + tile * (kThreads * 9), kTileBytes, &S.bar[s]);
+      }
+    }
+  }
+
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int stage = it % kStages;
+    const long long base = tile * kThreads;
+    const int cnt = (int)min((long long)kThreads, n - base);
+    double* sin_ = S.in[stage];
+    if (TMA && tile < full_tiles) {
+      mbar_wait(&S.bar[stage], (uint32_t)((it / kStages) & 1));
+    } else {
+      // coalesced cooperative load (non-TMA kernel, or the ragged last tile)
+      const double* src = a + base * 9;
+      const int nd = cnt * 9;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const int e = t + j * kThreads;
+        if (e < nd) sin_[e] = __ldg(src + e);
+      }
+      __syncthreads();
+    }
+    double m[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) m[j] = t < cnt ? sin_[t * 9 + j] : 0.0;
+    __syncthreads();  // stage fully consumed
+    if (TMA && t == 0) {
+      const long long nt = tile + (long long)kStages * gridDim.x;
+      if (nt < full_tiles) {
+        mbar_expect_tx(&S.bar[stage], kTileBytes);
+        bulk_load(S.in[stage], a + nt * (kThreads * 9), kTileBytes, &S.bar[stage]);
+      }
+    }
+
+    // ---- per-record arithmetic (registers only) ----
+    Inv v;
+    Lam L;
+    uint8_t f = 0;
+    if (MODE == kSym) {
+      if (not_symmetric(m)) {
+        f = EIG33_FLAG_NOT_SYMMETRIC;
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        v.i1 = v.j2 = v.j3 = v.disc = qnan;
+        L.l1 = L.l2 = L.l3 = qnan;
+      } else {
+        // mirror the upper triangle, src/eigensolver.cpp:108-111
+        m[3] = m[1];
+        m[6] = m[2];
+        m[7] = m[5];
+        v = invariants(m);
+        L = from_invariants(m, v, at_c, at_t, sc);
+      }
+    } else {
+      v = invariants(m);
+      if (MODE == kEig) {
+        L = from_invariants(m, v, at_c, at_t, sc);
+        if (v.disc < 0.0) f = kPending;
+      }
+    }
+
+    // ---- stage outputs, then contiguous stores ----
+    if (MODE != kInv && lam) {
+      S.lam[3 * t + 0] = L.l1;
+      S.lam[3 * t + 1] = L.l2;
+      S.lam[3 * t + 2] = L.l3;
+    }
+    if (inv) {
+      S.inv[4 * t + 0] = v.i1;
+      S.inv[4 * t + 1] = v.j2;
+      S.inv[4 * t + 2] = v.j3;
+      S.inv[4 * t + 3] = v.disc;
+    }
+    __syncthreads();
+    if (MODE != kInv && lam) {
+      double* dst = lam + base * 3;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int e = t + j * kThreads;
+        if (e < cnt * 3) dst[e] = S.lam[e];
+      }
+    }
+    if (inv) {
+      double* dst = inv + base * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int e = t + j * kThreads;
+        if (e < cnt * 4) dst[e] = S.inv[e];
+      }
+    }
+    if (MODE != kInv && flags && t < cnt) flags[base + t] = f;
+  }
+}
+
+// Deferred advisory: evaluate src/eigensolver.cpp:54 only where k_fused found
+// disc < 0.  Each block compacts a 2048-record window of pending flags into
+// SMEM, then its threads work the compacted list densely.
+constexpr int kAdvWindow = 2048;
+__global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict__ a, long long n,
+                                                       uint8_t* __restrict__ flags) {
+  __shared__ int list[kAdvWindow];
+  __shared__ int count;
+  for (long long w0 = (long long)blockIdx.x * kAdvWindow; w0 < n;
+       w0 += (long long)gridDim.x * kAdvWindow) {
+    if (threadIdx.x == 0) count = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kAdvWindow; i += blockDim.x) {
+      const long long idx = w0 + i;
+      const bool pend = idx < n && (flags[idx] & kPending);
+      const unsigned ballot = __ballot_sync(0xffffffffu, pend);
+      int base = 0;
+      if ((threadIdx.x & 31) == 0 && ballot) base = atomicAdd(&count, __popc(ballot));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (pend) list[base + __popc(ballot & ((1u << (threadIdx.x & 31)) - 1u))] = i;
+    }
+    __syncthreads();
+    const int c = count;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      const long long idx = w0 + list[j];
+      double m[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
+      const Inv v = invariants(m);
+      flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_triple_angle(const double* __restrict__ j3,
+                                                           const double* __restrict__ disc,
+                                                           long long n, double* __restrict__ phi) {
+  __shared__ double tab[kTabDoubles + 1];
+  load_tables(tab);
+  __syncthreads();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    phi[i] = triple_angle(j3[i], disc[i], tab, tab + EIG33_AT_N);
+}
+
+// ---------------------------------------------------------------------------
+// launch plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+static int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
+  g_err = what;
+  if (e != cudaSuccess) {
+    g_err += ": ";
+    g_err += cudaGetErrorString(e);
+  }
+  return code;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int occ[3][2] = {};
+  bool ready = false;
+};
+static DevInfo g_dev[64];
+
+template <int MODE, bool TMA>
+static int launch_fused(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
+                        cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDevice", e);
+  if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
+  DevInfo& d = g_dev[dev];
+  const size_t smem = sizeof(Smem);
+  auto kern = k_fused<MODE, TMA>;
+  if (!d.occ[MODE][TMA]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaFuncSetAttribute", e);
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    if (e != cudaSuccess) return fail(EIG33_ECUDA, "occupancy query", e);
+    if (!d.sms) {
+      e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return fail(EIG33_ECUDA, "SM count", e);
+    }
+    d.occ[MODE][TMA] = occ > 0 ? occ : 1;
+  }
+  const long long ntiles = (long long)((n + kThreads - 1) / kThreads);
+  const long long grid = ntiles < (long long)d.sms * d.occ[MODE][TMA]
+                             ? ntiles
+                             : (long long)d.sms * d.occ[MODE][TMA];
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_fused launch", e);
+  return EIG33_OK;
+}
+
+template <int MODE>
+static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
+                    cudaStream_t st) {
+  const bool aligned = ((uintptr_t)a & 15u) == 0;
+  return aligned ? launch_fused<MODE, true>(a, n, inv, lam, flags, st)
+                 : launch_fused<MODE, false>(a, n, inv, lam, flags, st);
+}
+
+static int launch_advisory(const double* a, size_t n, uint8_t* flags, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = g_dev[dev].sms;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long windows = (long long)((n + kAdvWindow - 1) / kAdvWindow);
+  const long long grid = windows < 4LL * sms ? windows : 4LL * sms;
+  k_advisory<<<(unsigned)grid, kThreads, 0, st>>>(a, (long long)n, flags);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_advisory launch", e);
+  return EIG33_OK;
+}
+
+}  // namespace eig33b
+
+using namespace eig33b;
+
+extern "C" {
+
+int eig33cu_version(void) { return (1 << 16) | 0; }
+const char* eig33cu_last_error(void) { return g_err.c_str(); }
+
+int eig33cu_invariants(const double* d_a, size_t n, double* d_inv, void* stream) {
+  g_err.clear();
+  if (n == 0) return EIG33_OK;
+  if (!d_a || !d_inv) return fail(EIG33_EINVAL, "eig33cu_invariants: null pointer");
+  return dispatch<kInv>(d_a, n, d_inv, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int eig33cu_eigvals(const double* d_a, size_t n, double* d_inv, double* d_lam, uint8_t* d_flags,
+                    void* stream) {
+  g_err.clear();
+  if (n == 0) return EIG33_OK;
+  if (!d_a || !d_lam) return fail(EIG33_EINVAL, "eig33cu_eigvals: null pointer");
+  int rc = dispatch<kEig>(d_a, n, d_inv, d_lam, d_flags, (cudaStream_t)stream);
+  if (rc == EIG33_OK && d_flags) rc = launch_advisory(d_a, n, d_flags, (cudaStream_t)stream);
+  return rc;
+}
+
+int eig33cu_eigvalss(const double* d_a, size_t n, double* d_inv, double* d_lam, uint8_t* d_flags,
+                     void* stream) {
+  g_err.clear();
+  if (n == 0) return EIG33_OK;
+  if (!d_a || !d_lam) return fail(EIG33_EINVAL, "eig33cu_eigvalss: null pointer");
+  return dispatch<kSym>(d_a, n, d_inv, d_lam, d_flags, (cudaStream_t)stream);
+}
+
+int eig33cu_triple_angle(const double* d_j3, const double* d_disc, size_t n, double* d_phi,
+                         void* stream) {
+  g_err.clear();
+  if (n == 0) return EIG33_OK;
+  if (!d_j3 || !d_disc || !d_phi) return fail(EIG33_EINVAL, "eig33cu_triple_angle: null pointer");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long blocks = (long long)((n + kThreads - 1) / kThreads);
+  const long long grid = blocks < 8LL * sms ? blocks : 8LL * sms;
+  k_triple_angle<<<(unsigned)grid, kThreads, 0, (cudaStream_t)stream>>>(d_j3, d_disc, (long long)n,
+                                                                       d_phi);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_triple_angle launch", e);
+  return EIG33_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// Builds against include/eig33/batch.hpp and runs the batched C++ API on the
+// GPU (tests/test_parity_gpu.py links it with _eig33cuda.so); checks a few
+// known answers from the reference tests and prints "OK".
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "eig33/batch.hpp"
+
+int main() {
+  std::vector<eig33::Mat3> a(3);
+  a[0].e = {-1, 0, 0, 0, 1, 0, 0, 0, 2};  // acceptance C1
+  a[1].e = {0, -1, 0, 1, 0, 0, 0, 0, 1};  // rotation: disc = -16, advisory
+  a[2].e = {7.25, 0, 0, 0, 7.25, 0, 0, 0, 7.25};
+  std::vector<eig33::InvariantSet> inv(3);
+  eig33::invariants(a.data(), a.size(), inv.data());
+  std::vector<eig33::EigenTriple> t(3);
+  eig33::eigvals(a.data(), a.size(), t.data());
+  bool ok = inv[0].disc == 36.0 && inv[0].i1 == 2.0 && inv[1].disc == -16.0 &&
+            t[1].non_real_advisory && !t[0].non_real_advisory && t[2].lambda1 == 7.25 &&
+            t[2].lambda3 == 7.25 && std::fabs(t[0].lambda3 - 2.0) < 1e-14;
+  bool threw = false;
+  try {
+    eig33::eigvalss(a.data() + 1, 1, t.data());
+  } catch (const eig33::NotSymmetric&) {
+    threw = true;
+  }
+  ok = ok && threw;
+  std::printf("%s\n", ok ? "OK" : "FAIL");
+  return ok ? 0 : 1;
+}

@@ -1,0 +1,107 @@
+"""CPU checks of the PRODUCT arithmetic (paper_2511_00292_b200/csrc/eig33_math.cuh
+compiled for the host by tests/hostmath): the same source the sm_100a kernels
+are built from, using only IEEE +,-,*,/,sqrt and explicit fma, so these
+properties carry over to the device (re-checked on the GPU in test_parity_gpu).
+"""
+import ctypes
+
+import mpmath
+import numpy as np
+import pytest
+
+from tests import _util as U
+
+
+def _call_unary(name, x, *extra):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    getattr(U.hostmath(), name)(U.ptr(x), U.S(x.size), *extra, U.ptr(out))
+    return out
+
+
+@pytest.mark.parametrize("c", [3, 6, 27])
+def test_const_division_is_ieee(c):
+    rng = np.random.default_rng(c)
+    n = 1 << 21
+    with np.errstate(all="ignore"):
+        x = rng.standard_normal(n) * np.ldexp(1.0, rng.integers(-1074, 1024, n))
+    tiny = np.ldexp(rng.random(1 << 16) + 1, rng.integers(-1074, -940, 1 << 16))
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+                         1.7976931348623157e308, -1.7976931348623157e308, 3.0, 27.0, 1.0])
+    x = np.concatenate([x, tiny, -tiny, specials])
+    q = _call_unary("hm_div", x, ctypes.c_int(c))
+    assert U.bit_equal(q, x / c).all()
+
+
+def _libm_atan2(y, x):
+    out = np.empty_like(y)
+    U.hostmath().hm_libm_atan2(U.ptr(y), U.ptr(x), U.S(y.size), U.ptr(out))
+    return out
+
+
+def _atan2(y, x):
+    out = np.empty_like(y)
+    U.hostmath().hm_atan2(U.ptr(y), U.ptr(x), U.S(y.size), U.ptr(out))
+    return out
+
+
+def test_atan2_special_values_match_glibc():
+    inf, nan = np.inf, np.nan
+    ys = np.array([0.0, 0.0, 0.0, 0.0, 1.0, 1.0, inf, inf, inf, 1.0, 1.0, 0.0, 5e-324, 1e-310, 1e300,
+                   1e-300, 1e308, 3.0])
+    xs = np.array([0.0, -0.0, 2.0, -2.0, 0.0, -0.0, inf, -inf, 1.0, inf, -inf, nan, 1e300, -1e-310,
+                   1e-300, -1e308, 1e-300, 3.0])
+    assert U.bit_equal(_atan2(ys, xs), _libm_atan2(ys, xs)).all()
+
+
+def test_atan2_correctly_rounded_and_within_1ulp_of_glibc():
+    rng = np.random.default_rng(5)
+    n = 1 << 21
+    y = np.abs(rng.standard_normal(n)) * np.exp(rng.uniform(-30, 30, n))
+    x = rng.standard_normal(n) * np.exp(rng.uniform(-30, 30, n))
+    ours, gl = _atan2(y, x), _libm_atan2(y, x)
+    d = np.abs(ours.view(np.int64) - gl.view(np.int64))
+    assert d.max() <= 1
+    assert (d == 0).mean() > 0.999
+    mpmath.mp.prec = 200
+    sample = np.concatenate([np.nonzero(d)[0][:100], rng.integers(0, n, 300)])
+    wrong = sum(float(mpmath.atan2(mpmath.mpf(y[i]), mpmath.mpf(x[i]))) != ours[i] for i in sample)
+    assert wrong <= 2  # correctly rounded except within ~2^-17 ulp of a midpoint
+
+
+def test_sincos_correctly_rounded_on_0_pi3():
+    rng = np.random.default_rng(6)
+    n = 1 << 21
+    th = rng.uniform(0, 1.0471975511965976, n)
+    th[:4096] = rng.uniform(0, 1e-3, 4096)
+    th[4096:4100] = [0.0, 1.0471975511965976, 5e-324, 2.0 ** -30]
+    s = np.empty(n); c = np.empty(n); gs = np.empty(n); gc = np.empty(n)
+    U.hostmath().hm_sincos(U.ptr(th), U.S(n), U.ptr(s), U.ptr(c))
+    U.hostmath().hm_libm_sincos(U.ptr(th), U.S(n), U.ptr(gs), U.ptr(gc))
+    for ours, gl in ((s, gs), (c, gc)):
+        d = np.abs(ours.view(np.int64) - gl.view(np.int64))
+        assert d.max() <= 1 and (d == 0).mean() > 0.997
+    mpmath.mp.prec = 200
+    wrong = 0
+    for i in rng.integers(0, n, 400):
+        wrong += float(mpmath.sin(mpmath.mpf(th[i]))) != s[i]
+        wrong += float(mpmath.cos(mpmath.mpf(th[i]))) != c[i]
+    assert wrong <= 1
+    nan_s = np.empty(1); nan_c = np.empty(1)
+    U.hostmath().hm_sincos(U.ptr(np.array([np.nan])), U.S(1), U.ptr(nan_s), U.ptr(nan_c))
+    assert np.isnan(nan_s[0]) and np.isnan(nan_c[0])
+
+
+def test_product_math_parity_vs_checker():
+    a = U.mixed_corpus(1 << 19, 11)
+    n = a.shape[0]
+    inv = np.empty((n, 4))
+    U.hostmath().hm_invariants(U.ptr(a), U.S(n), U.ptr(inv))
+    assert U.bit_equal(inv, U.checker_invariants(a)).all()
+    lam = np.empty((n, 3)); adv = np.empty(n, np.uint8)
+    U.hostmath().hm_eigvals(U.ptr(a), U.S(n), U.ptr(lam), U.ptr(adv))
+    lam_r, adv_r = U.checker_eigvals(a)
+    assert (adv == adv_r).all()
+    err = U.lam_error_units(lam, lam_r)
+    assert err.max() <= U.TOL_UNITS
+    assert (err == 0).mean() > 0.995

@@ -1,0 +1,240 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the
+checker (compiled reference core when present, else the C restatement), run
+on this box's host cores in the same process (lambda bits depend on the host
+libm -- SURVEY 0.6).
+
+Gates (BASELINE north_star): invariants bit-exact (NaN == NaN), advisory and
+NotSymmetric flags bit-exact, lambda within 4 * 2^-52 * max|lambda_ref|
+(TOL_UNITS) with identical non-finite classes; config 4 (ill-conditioned
+eigenbasis) falls back to the reference's own forward error where the 4-ulp
+test fails (tests/_exact.py).
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests import _util as U
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2511_00292_b200 as eig  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "eig33_golden.npz")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")  # loud: no silent CPU pass
+    eig.lib()
+    yield
+    torch.cuda.synchronize()
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 9)).cuda()
+
+
+def _run(a_host, *, inv=True, flags=True):
+    r = eig.eigvals(_dev(a_host), return_invariants=inv, return_flags=flags)
+    torch.cuda.synchronize()
+    return [None if x is None else x.cpu().numpy() for x in r]
+
+
+def _assert_parity(a, lam, inv, flags, name, max_units=U.TOL_UNITS, lam_tol_fallback=None):
+    inv_r = U.checker_invariants(a)
+    bad = ~U.bit_equal(inv, inv_r).all(axis=1)
+    assert not bad.any(), f"{name}: {bad.sum()} invariant rows differ, first {np.nonzero(bad)[0][:5]}"
+    lam_r, adv_r = U.checker_eigvals(a)
+    if flags is not None:
+        fb = (flags & eig.FLAG_ADVISORY) != adv_r
+        assert not fb.any(), f"{name}: advisory differs on {fb.sum()} records"
+    err = U.lam_error_units(lam, lam_r)
+    over = err > max_units
+    if over.any() and lam_tol_fallback is not None:
+        over[over] = ~lam_tol_fallback(a[over], lam[over], lam_r[over])
+    assert not over.any(), (f"{name}: {over.sum()} records over {max_units} units; worst "
+                            f"{np.max(err):.3g} at {np.argmax(err)}")
+    return err
+
+
+def test_golden_fixtures_on_device():
+    g = np.load(GOLDEN)
+    lam, inv, flags = _run(g["a"])
+    assert U.bit_equal(inv, g["inv"]).all()
+    assert ((flags & 1) == g["adv"]).all()
+    assert (U.lam_error_units(lam, g["lam"]) <= U.TOL_UNITS).all()
+    _assert_parity(g["a"], lam, inv, flags, "golden")
+
+
+def test_known_answers_on_device():
+    a = np.array([U.KAT_MATRICES[k] for k in ("diag(-1,1,2)", "diag(1,2,3)", "rotation", "7.25*I")]
+                 + [U.perf_matrix()], dtype=np.float64)
+    lam, inv, flags = _run(a)
+    assert inv[0][3] == 36.0 and inv[0][0] == 2.0
+    assert inv[1][1] == 1.0 and inv[1][2] == 0.0
+    assert inv[2][3] == -16.0 and flags[2] & 1 and np.isfinite(lam[2]).all()
+    assert (lam[3] == 7.25).all()
+    assert np.abs(lam[1] - [1, 2, 3]).max() <= 1e-14
+    assert [np.float64(x).view(np.uint64) for x in inv[4]] == [
+        0x3FF000000000002C, 0x3FF5555555555573, 0xBFE2F684BDA12F8F, 0x3A5F620000000030]
+
+
+def test_triple_angle_kats():
+    ta = np.load(GOLDEN)
+    j3 = torch.tensor(ta["ta_in"][:, 0], dtype=torch.float64, device="cuda")
+    dc = torch.tensor(ta["ta_in"][:, 1], dtype=torch.float64, device="cuda")
+    phi = eig.triple_angle(j3, dc).cpu().numpy()
+    assert U.bit_equal(phi, ta["ta"]).all()
+    assert phi[0] == np.pi / 2 and phi[1] == 0.0 and phi[2] == np.pi and phi[3] == 0.0
+
+
+@pytest.mark.parametrize("config,n", [(1, 1 << 20), (2, 1 << 22), (3, 1 << 22), (4, 1 << 22),
+                                      (5, 1 << 22)])
+def test_config_parity_full_size(config, n):
+    """BASELINE configs at their full batch (config 3 at 2^22 of its 2^28; the
+    full 2^28 is covered by test_config3_full_properties)."""
+    a_d = eig.generate(config, n, seed=1000 + config)
+    r = eig.eigvals(a_d, return_invariants=True, return_flags=True)
+    torch.cuda.synchronize()
+    a = a_d.cpu().numpy()
+    lam, inv, flags = (x.cpu().numpy() for x in r)
+    fallback = None
+    if config == 4:
+        from tests import _exact
+        fallback = _exact.within_reference_forward_error
+    err = _assert_parity(a, lam, inv, flags, f"config{config}", lam_tol_fallback=fallback)
+    assert (err == 0).mean() > 0.99  # most records reproduce the reference bits exactly
+
+
+def test_config3_full_properties():
+    """2^28 records (19.3 GB in): size-independent properties on every record
+    (ascending order, trace consistency per proj/tests/test_eigensolver.cpp:83-102)
+    plus exact parity on a strided sample."""
+    n = 1 << 28
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * (72 + 24 + 8) + (4 << 30):
+        pytest.skip("not enough device memory for the 2^28 batch")
+    a_d = eig.generate(3, n, seed=3)
+    lam = eig.eigvals(a_d).lam
+    l1, l2, l3 = lam[:, 0], lam[:, 1], lam[:, 2]
+    assert bool(((l1 <= l2) & (l2 <= l3)).all())
+    a9 = a_d.view(n, 9)
+    i1 = (a9[:, 0] + a9[:, 4]) + a9[:, 8]
+    s = (l1 + l2) + l3
+    spread = l3 - l1
+    bound = 20 * 2.0 ** -53 * (i1.abs() + 2 * spread)
+    assert bool(((s - i1).abs() <= bound).all())
+    idx = torch.arange(0, n, 977, device="cuda")
+    a_s = a9[idx].cpu().numpy()
+    _assert_parity(a_s, lam[idx].cpu().numpy(), eig.invariants(a9[idx]).cpu().numpy(), None, "c3-sample")
+    del a_d, lam
+
+
+def test_mixed_corpus_and_nonfinite_classes():
+    a = U.mixed_corpus(1 << 20, 17)
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, "mixed")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 255, 256, 257, 511, 4097, 100003])
+def test_ragged_sizes_and_tails(n):
+    a = U.mixed_corpus(max(n, 8), n)[:n]
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, f"n={n}")
+
+
+def test_empty_batch():
+    r = eig.eigvals(torch.empty((0, 9), dtype=torch.float64, device="cuda"), return_invariants=True)
+    assert r.lam.shape == (0, 3) and r.inv.shape == (0, 4)
+
+
+def test_misaligned_input_uses_coalesced_path():
+    n = 70001
+    a = U.mixed_corpus(n, 5)
+    buf = torch.empty(n * 9 + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(a.reshape(-1)).cuda()
+    view = buf[1:].view(n, 9)  # 8-B aligned, not 16-B: no TMA
+    assert view.data_ptr() % 16 == 8
+    r = eig.eigvals(view, return_invariants=True, return_flags=True)
+    torch.cuda.synchronize()
+    _assert_parity(a, r.lam.cpu().numpy(), r.inv.cpu().numpy(), r.flags.cpu().numpy(), "misaligned")
+
+
+def test_invariants_only_entry_point():
+    a_d = eig.generate(5, 1 << 21, seed=9)
+    inv = eig.invariants(a_d).cpu().numpy()
+    assert U.bit_equal(inv, U.checker_invariants(a_d.cpu().numpy())).all()
+
+
+def test_eigvalss_device_and_host():
+    a_d = eig.generate(1, 1 << 20, seed=77)  # bitwise symmetric
+    r_s = eig.eigvalss(a_d, return_invariants=True, return_flags=True)
+    r_g = eig.eigvals(a_d, return_invariants=True)
+    torch.cuda.synchronize()
+    assert U.bit_equal(r_s.lam.cpu().numpy(), r_g.lam.cpu().numpy()).all()
+    assert (r_s.flags.cpu().numpy() == 0).all()
+    lam_r, st_r = U.checker_eigvalss(a_d.cpu().numpy())
+    assert (st_r == 0).all()
+    assert (U.lam_error_units(r_s.lam.cpu().numpy(), lam_r) <= U.TOL_UNITS).all()
+    # symmetry gate (test_eigensolver.cpp:150-165) -> flag bit1 on device, ValueError on host
+    bad = np.array([[1.0, 1.0, 0, 1.0 + 1e-8, 2, 0, 0, 0, 3], U.KAT_MATRICES["rotation"],
+                    [1.0, 1.0, 0, 1.0 + 2.0 ** -52, 2, 0, 0, 0, 3]])
+    r = eig.eigvalss(_dev(bad), return_flags=True)
+    f = r.flags.cpu().numpy()
+    assert list((f & eig.FLAG_NOT_SYMMETRIC) != 0) == [True, True, False]
+    with pytest.raises(ValueError):
+        eig.eigvalss(bad)
+    lam_h = eig.eigvalss(bad[2:]).lam
+    lam_c, _ = U.checker_eigvalss(bad[2:])
+    assert (U.lam_error_units(lam_h, lam_c) <= U.TOL_UNITS).all()
+
+
+def test_host_entry_points_equal_device_entry_points():
+    a_d = eig.generate(3, (1 << 22) + 5, seed=42)
+    r_d = eig.eigvals(a_d, return_invariants=True, return_flags=True)
+    a = a_d.cpu().numpy()
+    r_h = eig.eigvals(a, return_invariants=True, return_flags=True)
+    assert U.bit_equal(r_h.lam, r_d.lam.cpu().numpy()).all()
+    assert U.bit_equal(r_h.inv, r_d.inv.cpu().numpy()).all()
+    assert (r_h.flags == r_d.flags.cpu().numpy()).all()
+    r_m = eig.multi_eigvals(a, 1, return_invariants=True)
+    assert U.bit_equal(r_m.lam, r_h.lam).all()
+    assert U.bit_equal(eig.invariants(a), r_h.inv).all()
+
+
+def test_shard_invariance_bitwise():
+    """Results are identical whatever the contiguous even-aligned sharding
+    (the multi-GPU driver's partition), emulated on one device."""
+    n = 3_000_001
+    a_d = eig.generate(5, n, seed=5)
+    full = eig.eigvals(a_d, return_invariants=True).lam
+    for g in (2, 4, 8):
+        bounds = [2 * (k * n // (2 * g)) for k in range(g)] + [n]
+        parts = [eig.eigvals(a_d[lo:hi]).lam for lo, hi in zip(bounds[:-1], bounds[1:])]
+        assert torch.equal(torch.cat(parts).view(torch.int64), full.view(torch.int64))
+
+
+def test_generator_is_counter_based():
+    a = eig.generate(3, 1 << 16, seed=11)
+    b = eig.generate(3, 1 << 15, seed=11, first_index=1 << 15)
+    assert torch.equal(a[1 << 15:], b)
+    c1 = eig.generate(1, 4096, seed=1).cpu().numpy()
+    assert (c1[:, [3, 6, 7]] == c1[:, [1, 2, 5]]).all()  # bitwise symmetric
+
+
+def test_cxx_batch_api_links_and_runs(tmp_path):
+    exe = tmp_path / "batch_api_check"
+    src = os.path.join(U.ROOT, "tests", "cpp", "batch_api_check.cpp")
+    so_dir = os.path.join(U.ROOT, "paper_2511_00292_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-DEIG33_STANDALONE_TYPES", "-I",
+                        os.path.join(U.ROOT, "include"), src, "-o", str(exe),
+                        os.path.join(so_dir, "_eig33cuda.so"), "-Wl,-rpath," + so_dir],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "OK", out.stdout + out.stderr

@@ -31,7 +31,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "_eig33cuda.so")
+_SO = os.environ.get("EIG33_SO") or os.path.join(_HERE, "_eig33cuda.so")
 
 eps_mach = 2.0 ** -53  # reference include/eig33/mat3.hpp:10
 FLAG_ADVISORY = 0x1

@@ -77,6 +77,24 @@ def build_product(force=False):
     return SO
 
 
+def build_variant(name, defines):
+    """Experimental build with extra -D flags into build/variants/<name>.so
+    (selected at run time with EIG33_SO=...); the product is build_product()."""
+    out_dir = os.path.join(HERE, "build", "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    for s in SOURCES:
+        o = os.path.join(out_dir, f"{name}_{s}.o")
+        _run([nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o],
+             log=os.path.join(out_dir, f"{name}_{s}.log"))
+        objs.append(o)
+    so = os.path.join(out_dir, name + ".so")
+    _run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", so, *objs,
+          "-Xcompiler", "-pthread"])
+    return so
+
+
 def build_oracle():
     make = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"]
     _run(make)

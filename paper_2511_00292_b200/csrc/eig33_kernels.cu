@@ -34,6 +34,10 @@ namespace eig33b {
 
 constexpr int kThreads = 256;  // records per tile == threads per block
 constexpr int kStages = 2;     // TMA ring depth
+#ifndef EIG33_MIN_BLOCKS
+#define EIG33_MIN_BLOCKS 3
+#endif
+constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
 constexpr int kTabDoubles = EIG33_AT_N + 4 * EIG33_AT_N * 2 + EIG33_SC_N * 5;  // 243
 constexpr uint32_t kTileBytes = kThreads * 9 * sizeof(double);                 // 18432
 constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
@@ -42,8 +46,6 @@ enum Mode { kEig = 0, kInv = 1, kSym = 2 };
 
 struct __align__(16) Smem {
   double in[kStages][kThreads * 9];
-  double lam[kThreads * 3];
-  double inv[kThreads * 4];
   double tab[kTabDoubles + 1];
   unsigned long long bar[kStages];
 };
@@ -93,9 +95,45 @@ __device__ __forceinline__ void load_tables(double* tab) {
   }
 }
 
-// Persistent fused kernel.  One tile = kThreads consecutive records.
-template <int MODE, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2)
+struct Tabs {
+  const double *at_c, *at_t, *sc;
+};
+
+// One record: moderate records (every |a_ij| in [2^-60,2^60), the common
+// case) take the guard-free CSE path; everything else (zeros, subnormals,
+// extreme exponents, inf/NaN) takes the checked reference-order path.  Both
+// produce the reference's bits; only their cost differs.
+template <int MODE, bool WANT_FLAGS>
+__device__ __forceinline__ void record(double m[9], const Tabs& T, Inv& v, Lam& L, uint8_t& f) {
+  f = 0;
+  if (MODE == kSym) {
+    if (not_symmetric(m)) {
+      f = EIG33_FLAG_NOT_SYMMETRIC;
+      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+      v.i1 = v.j2 = v.j3 = v.disc = qnan;
+      L.l1 = L.l2 = L.l3 = qnan;
+      return;
+    }
+    // mirror the upper triangle, src/eigensolver.cpp:108-111
+    m[3] = m[1];
+    m[6] = m[2];
+    m[7] = m[5];
+  }
+  if (is_moderate(m)) {
+    v = invariants_moderate(m);
+    if (MODE != kInv) L = from_invariants_moderate(m, v, T.at_c, T.at_t, T.sc);
+  } else {
+    v = invariants(m);
+    if (MODE != kInv) L = from_invariants(m, v, T.at_c, T.at_t, T.sc);
+  }
+  if (MODE == kEig && WANT_FLAGS && v.disc < 0.0) f = kPending;
+}
+
+// Persistent fused kernel.  One tile = kThreads consecutive records, one per
+// thread; outputs go straight from registers to HBM (each warp's stores cover
+// a contiguous 768-B lambda run / 1-KB invariant run, merged in L2).
+template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
             double* __restrict__ lam, uint8_t* __restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -110,9 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   load_tables(S.tab);
   __syncthreads();
-  const double* at_c = S.tab;
-  const double* at_t = S.tab + EIG33_AT_N;
-  const double* sc = S.tab + 9 * EIG33_AT_N;
+  const Tabs T{S.tab, S.tab + EIG33_AT_N, S.tab + 9 * EIG33_AT_N};
 
   if (TMA && t == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -145,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     double m[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) m[j] = t < cnt ? sin_[t * 9 + j] : 0.0;
+    for (int j = 0; j < 9; ++j) m[j] = sin_[t * 9 + j];
     __syncthreads();  // stage fully consumed
     if (TMA && t == 0) {
       const long long nt = tile + (long long)kStages * gridDim.x;
@@ -154,63 +190,26 @@ __global__ void __launch_bounds__(kThreads, 2)
         bulk_load(S.in[stage], a + nt * (kThreads * 9), kTileBytes, &S.bar[stage]);
       }
     }
+    if (t >= cnt) continue;  // ragged tail (last tile only; no barrier follows)
 
-    // ---- per-record arithmetic (registers only) ----
     Inv v;
     Lam L;
-    uint8_t f = 0;
-    if (MODE == kSym) {
-      if (not_symmetric(m)) {
-        f = EIG33_FLAG_NOT_SYMMETRIC;
-        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-        v.i1 = v.j2 = v.j3 = v.disc = qnan;
-        L.l1 = L.l2 = L.l3 = qnan;
-      } else {
-        // mirror the upper triangle, src/eigensolver.cpp:108-111
-        m[3] = m[1];
-        m[6] = m[2];
-        m[7] = m[5];
-        v = invariants(m);
-        L = from_invariants(m, v, at_c, at_t, sc);
-      }
-    } else {
-      v = invariants(m);
-      if (MODE == kEig) {
-        L = from_invariants(m, v, at_c, at_t, sc);
-        if (v.disc < 0.0) f = kPending;
-      }
-    }
+    uint8_t f;
+    record<MODE, WANT_FLAGS>(m, T, v, L, f);
 
-    // ---- stage outputs, then contiguous stores ----
-    if (MODE != kInv && lam) {
-      S.lam[3 * t + 0] = L.l1;
-      S.lam[3 * t + 1] = L.l2;
-      S.lam[3 * t + 2] = L.l3;
+    const long long r = base + t;
+    if (MODE != kInv) {
+      lam[r * 3 + 0] = L.l1;
+      lam[r * 3 + 1] = L.l2;
+      lam[r * 3 + 2] = L.l3;
     }
-    if (inv) {
-      S.inv[4 * t + 0] = v.i1;
-      S.inv[4 * t + 1] = v.j2;
-      S.inv[4 * t + 2] = v.j3;
-      S.inv[4 * t + 3] = v.disc;
+    if (WANT_INV) {
+      inv[r * 4 + 0] = v.i1;
+      inv[r * 4 + 1] = v.j2;
+      inv[r * 4 + 2] = v.j3;
+      inv[r * 4 + 3] = v.disc;
     }
-    __syncthreads();
-    if (MODE != kInv && lam) {
-      double* dst = lam + base * 3;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int e = t + j * kThreads;
-        if (e < cnt * 3) dst[e] = S.lam[e];
-      }
-    }
-    if (inv) {
-      double* dst = inv + base * 4;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int e = t + j * kThreads;
-        if (e < cnt * 4) dst[e] = S.inv[e];
-      }
-    }
-    if (MODE != kInv && flags && t < cnt) flags[base + t] = f;
+    if (MODE != kInv && WANT_FLAGS) flags[r] = f;
   }
 }
 
@@ -277,12 +276,11 @@ static int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
 
 struct DevInfo {
   int sms = 0;
-  int occ[3][2] = {};
-  bool ready = false;
+  int occ[3][2][2][2] = {};
 };
 static DevInfo g_dev[64];
 
-template <int MODE, bool TMA>
+template <int MODE, bool TMA, bool WI, bool WF>
 static int launch_fused(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
                         cudaStream_t st) {
   int dev = 0;
@@ -291,35 +289,46 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
   DevInfo& d = g_dev[dev];
   const size_t smem = sizeof(Smem);
-  auto kern = k_fused<MODE, TMA>;
-  if (!d.occ[MODE][TMA]) {
+  auto kern = k_fused<MODE, TMA, WI, WF>;
+  int& occ = d.occ[MODE][TMA][WI][WF];
+  if (!occ) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaFuncSetAttribute", e);
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "occupancy query", e);
     if (!d.sms) {
       e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
       if (e != cudaSuccess) return fail(EIG33_ECUDA, "SM count", e);
     }
-    d.occ[MODE][TMA] = occ > 0 ? occ : 1;
+    occ = o > 0 ? o : 1;
   }
   const long long ntiles = (long long)((n + kThreads - 1) / kThreads);
-  const long long grid = ntiles < (long long)d.sms * d.occ[MODE][TMA]
-                             ? ntiles
-                             : (long long)d.sms * d.occ[MODE][TMA];
+  const long long cap = (long long)d.sms * occ;
+  const long long grid = ntiles < cap ? ntiles : cap;
   kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_fused launch", e);
   return EIG33_OK;
 }
 
+template <int MODE, bool TMA>
+static int dispatch_out(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
+                        cudaStream_t st) {
+  if (inv) {
+    return flags ? launch_fused<MODE, TMA, true, true>(a, n, inv, lam, flags, st)
+                 : launch_fused<MODE, TMA, true, false>(a, n, inv, lam, flags, st);
+  }
+  return flags ? launch_fused<MODE, TMA, false, true>(a, n, inv, lam, flags, st)
+               : launch_fused<MODE, TMA, false, false>(a, n, inv, lam, flags, st);
+}
+
 template <int MODE>
 static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
                     cudaStream_t st) {
   const bool aligned = ((uintptr_t)a & 15u) == 0;
-  return aligned ? launch_fused<MODE, true>(a, n, inv, lam, flags, st)
-                 : launch_fused<MODE, false>(a, n, inv, lam, flags, st);
+  return aligned ? dispatch_out<MODE, true>(a, n, inv, lam, flags, st)
+                 : dispatch_out<MODE, false>(a, n, inv, lam, flags, st);
 }
 
 static int launch_advisory(const double* a, size_t n, uint8_t* flags, cudaStream_t st) {

@@ -11,16 +11,41 @@
 using namespace eig33b;
 
 extern "C" {
+// path: 0 = dispatch like the kernel (moderate fast path when is_moderate),
+//       1 = always the checked general path, 2 = always the moderate path
+static Inv inv_path(const double* m, int path) {
+  if (path == 2 || (path == 0 && is_moderate(m))) return invariants_moderate(m);
+  return invariants(m);
+}
+static Lam lam_path(const double* m, const Inv& v, int path) {
+  if (path == 2 || (path == 0 && is_moderate(m)))
+    return from_invariants_moderate(m, v, eig33_at_c, eig33_at_t, eig33_sc);
+  return from_invariants(m, v, eig33_at_c, eig33_at_t, eig33_sc);
+}
+int hm_is_moderate(const double* a) { return is_moderate(a) ? 1 : 0; }
+void hm_invariants_path(const double* a, size_t n, double* inv, int path) {
+  for (size_t i = 0; i < n; ++i) {
+    const Inv v = inv_path(a + 9 * i, path);
+    inv[4 * i] = v.i1; inv[4 * i + 1] = v.j2; inv[4 * i + 2] = v.j3; inv[4 * i + 3] = v.disc;
+  }
+}
+void hm_eigvals_path(const double* a, size_t n, double* lam, int path) {
+  for (size_t i = 0; i < n; ++i) {
+    const Inv v = inv_path(a + 9 * i, path);
+    const Lam l = lam_path(a + 9 * i, v, path);
+    lam[3 * i] = l.l1; lam[3 * i + 1] = l.l2; lam[3 * i + 2] = l.l3;
+  }
+}
 void hm_invariants(const double* a, size_t n, double* inv) {
   for (size_t i = 0; i < n; ++i) {
-    const Inv v = invariants(a + 9 * i);
+    const Inv v = inv_path(a + 9 * i, 0);
     inv[4 * i] = v.i1; inv[4 * i + 1] = v.j2; inv[4 * i + 2] = v.j3; inv[4 * i + 3] = v.disc;
   }
 }
 void hm_eigvals(const double* a, size_t n, double* lam, uint8_t* adv) {
   for (size_t i = 0; i < n; ++i) {
-    const Inv v = invariants(a + 9 * i);
-    const Lam l = from_invariants(a + 9 * i, v, eig33_at_c, eig33_at_t, eig33_sc);
+    const Inv v = inv_path(a + 9 * i, 0);
+    const Lam l = lam_path(a + 9 * i, v, 0);
     lam[3 * i] = l.l1; lam[3 * i + 1] = l.l2; lam[3 * i + 2] = l.l3;
     if (adv) adv[i] = advisory(a + 9 * i, v) ? 1 : 0;
   }

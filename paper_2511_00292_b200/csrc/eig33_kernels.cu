@@ -32,22 +32,27 @@
 
 namespace eig33b {
 
-constexpr int kThreads = 256;  // records per tile == threads per block
-constexpr int kStages = 2;     // TMA ring depth
+constexpr int kThreads = 256;  // threads per block (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 32;     // records per warp chunk (one per lane)
+#ifndef EIG33_STAGES
+#define EIG33_STAGES 3
+#endif
+constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth
 #ifndef EIG33_MIN_BLOCKS
-#define EIG33_MIN_BLOCKS 3
+#define EIG33_MIN_BLOCKS 2
 #endif
 constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
 constexpr int kTabDoubles = EIG33_AT_N + 4 * EIG33_AT_N * 2 + EIG33_SC_N * 5;  // 243
-constexpr uint32_t kTileBytes = kThreads * 9 * sizeof(double);                 // 18432
+constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);                  // 2304
 constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
 
 enum Mode { kEig = 0, kInv = 1, kSym = 2 };
 
 struct __align__(16) Smem {
-  double in[kStages][kThreads * 9];
+  double in[kWarps][kStages][kChunk * 9];
   double tab[kTabDoubles + 1];
-  unsigned long long bar[kStages];
+  unsigned long long bar[kWarps][kStages];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -104,7 +109,8 @@ struct Tabs {
 // extreme exponents, inf/NaN) takes the checked reference-order path.  Both
 // produce the reference's bits; only their cost differs.
 template <int MODE, bool WANT_FLAGS>
-__device__ __forceinline__ void record(double m[9], const Tabs& T, Inv& v, Lam& L, uint8_t& f) {
+__device__ __forceinline__ void record(double m[9], bool mod, const Tabs& T, Inv& v, Lam& L,
+                                       uint8_t& f) {
   f = 0;
   if (MODE == kSym) {
     if (not_symmetric(m)) {
@@ -118,8 +124,9 @@ __device__ __forceinline__ void record(double m[9], const Tabs& T, Inv& v, Lam& 
     m[3] = m[1];
     m[6] = m[2];
     m[7] = m[5];
+    mod = is_moderate(m);
   }
-  if (is_moderate(m)) {
+  if (mod) {
     v = invariants_moderate(m);
     if (MODE != kInv) L = from_invariants_moderate(m, v, T.at_c, T.at_t, T.sc);
   } else {
@@ -129,75 +136,84 @@ __device__ __forceinline__ void record(double m[9], const Tabs& T, Inv& v, Lam& 
   if (MODE == kEig && WANT_FLAGS && v.disc < 0.0) f = kPending;
 }
 
-// Persistent fused kernel.  One tile = kThreads consecutive records, one per
-// thread; outputs go straight from registers to HBM (each warp's stores cover
-// a contiguous 768-B lambda run / 1-KB invariant run, merged in L2).
+// Persistent fused kernel.  Work unit = a chunk of 32 consecutive records, one
+// per lane.  Every warp runs its own pipeline: lane 0 streams the warp's
+// chunks HBM -> SMEM with cp.async.bulk into a kStages-deep per-warp ring
+// completed on per-warp mbarriers, so there is no block-wide barrier in the
+// loop and warps drift into different phases (invariants vs transcendentals),
+// which is what keeps the FP64 pipe fed.  Outputs go straight from registers
+// to HBM (a warp's stores cover one contiguous 768-B lambda run).
 template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
             double* __restrict__ lam, uint8_t* __restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  const int t = threadIdx.x;
-  const long long ntiles = (n + kThreads - 1) / kThreads;
-  const long long full_tiles = n / kThreads;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long nchunks = (n + kChunk - 1) / kChunk;
+  const long long full = n / kChunk;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  const long long W = (long long)gridDim.x * kWarps;
+  double* ring = S.in[warp][0];
+  unsigned long long* bars = S.bar[warp];
 
-  if (TMA && t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+  if (TMA && lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_tables(S.tab);
-  __syncthreads();
+  __syncthreads();  // tables + barrier init; the only block-wide barrier
   const Tabs T{S.tab, S.tab + EIG33_AT_N, S.tab + 9 * EIG33_AT_N};
 
-  if (TMA && t == 0) {
+  if (TMA && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      const long long tile = blockIdx.x + (long long)s * gridDim.x;
-      if (tile < full_tiles) {
-        mbar_expect_tx(&S.bar[s], kTileBytes);
-        bulk_load(S.in[s], a + tile * (kThreads * 9), kTileBytes, &S.bar[s]);
+      const long long c = gw + (long long)s * W;
+      if (c < full) {
+        mbar_expect_tx(&bars[s], kChunkBytes);
+        bulk_load(ring + s * (kChunk * 9), a + c * (kChunk * 9), kChunkBytes, &bars[s]);
       }
     }
   }
 
   int it = 0;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (long long c = gw; c < nchunks; c += W, ++it) {
     const int stage = it % kStages;
-    const long long base = tile * kThreads;
-    const int cnt = (int)min((long long)kThreads, n - base);
-    double* sin_ = S.in[stage];
-    if (TMA && tile < full_tiles) {
-      mbar_wait(&S.bar[stage], (uint32_t)((it / kStages) & 1));
+    double* buf = ring + stage * (kChunk * 9);
+    const long long base = c * kChunk;
+    const int cnt = (int)min((long long)kChunk, n - base);
+    if (TMA && c < full) {
+      mbar_wait(&bars[stage], (uint32_t)((it / kStages) & 1));
     } else {
-      // coalesced cooperative load (non-TMA kernel, or the ragged last tile)
+      // coalesced cooperative load: misaligned input, or the ragged last chunk
       const double* src = a + base * 9;
-      const int nd = cnt * 9;
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
-        const int e = t + j * kThreads;
-        if (e < nd) sin_[e] = __ldg(src + e);
+        const int e = lane + 32 * j;
+        if (e < cnt * 9) buf[e] = __ldg(src + e);
       }
-      __syncthreads();
+      __syncwarp();
     }
     double m[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) m[j] = sin_[t * 9 + j];
-    __syncthreads();  // stage fully consumed
-    if (TMA && t == 0) {
-      const long long nt = tile + (long long)kStages * gridDim.x;
-      if (nt < full_tiles) {
-        mbar_expect_tx(&S.bar[stage], kTileBytes);
-        bulk_load(S.in[stage], a + nt * (kThreads * 9), kTileBytes, &S.bar[stage]);
+    for (int j = 0; j < 9; ++j) m[j] = buf[lane * 9 + j];
+    // consume all nine loads before the stage is handed back to the TMA engine
+    const bool mod = is_moderate(m);
+    __syncwarp();
+    if (TMA && lane == 0) {
+      const long long nc = c + (long long)kStages * W;
+      if (nc < full) {
+        mbar_expect_tx(&bars[stage], kChunkBytes);
+        bulk_load(buf, a + nc * (kChunk * 9), kChunkBytes, &bars[stage]);
       }
     }
-    if (t >= cnt) continue;  // ragged tail (last tile only; no barrier follows)
+    if (lane >= cnt) continue;  // ragged tail (last chunk only)
 
     Inv v;
     Lam L;
     uint8_t f;
-    record<MODE, WANT_FLAGS>(m, T, v, L, f);
+    record<MODE, WANT_FLAGS>(m, mod, T, v, L, f);
 
-    const long long r = base + t;
+    const long long r = base + lane;
     if (MODE != kInv) {
       lam[r * 3 + 0] = L.l1;
       lam[r * 3 + 1] = L.l2;
@@ -303,9 +319,9 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
     }
     occ = o > 0 ? o : 1;
   }
-  const long long ntiles = (long long)((n + kThreads - 1) / kThreads);
+  const long long nblk = (long long)((n + kThreads - 1) / kThreads);  // one chunk per warp
   const long long cap = (long long)d.sms * occ;
-  const long long grid = ntiles < cap ? ntiles : cap;
+  const long long grid = nblk < cap ? nblk : cap;
   kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_fused launch", e);

@@ -32,7 +32,10 @@
 
 namespace eig33b {
 
-constexpr int kThreads = 256;  // threads per block (8 warps)
+#ifndef EIG33_THREADS
+#define EIG33_THREADS 256
+#endif
+constexpr int kThreads = EIG33_THREADS;  // threads per block
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 32;     // records per warp chunk (one per lane)
 #ifndef EIG33_STAGES
@@ -104,45 +107,110 @@ struct Tabs {
   const double *at_c, *at_t, *sc;
 };
 
-// One record: moderate records (every |a_ij| in [2^-60,2^60), the common
-// case) take the guard-free CSE path; everything else (zeros, subnormals,
-// extreme exponents, inf/NaN) takes the checked reference-order path.  Both
-// produce the reference's bits; only their cost differs.
+// Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
+// the eigen-stage carry.  Moderate records (every |a_ij| in [2^-60,2^60), the
+// common case) use the CSE DAG; the rest the checked reference-order kernel.
+// Both produce the reference's bits.
 template <int MODE, bool WANT_FLAGS>
-__device__ __forceinline__ void record(double m[9], bool mod, const Tabs& T, Inv& v, Lam& L,
-                                       uint8_t& f) {
+__device__ __forceinline__ void stage1(double m[9], bool& mod, Inv& v, Carry& c, uint8_t& f,
+                                       bool& bad) {
   f = 0;
+  bad = false;
   if (MODE == kSym) {
     if (not_symmetric(m)) {
+      bad = true;
+      mod = false;
       f = EIG33_FLAG_NOT_SYMMETRIC;
-      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-      v.i1 = v.j2 = v.j3 = v.disc = qnan;
-      L.l1 = L.l2 = L.l3 = qnan;
-      return;
     }
-    // mirror the upper triangle, src/eigensolver.cpp:108-111
-    m[3] = m[1];
+    m[3] = m[1];  // mirror the upper triangle, src/eigensolver.cpp:108-111
     m[6] = m[2];
     m[7] = m[5];
-    mod = is_moderate(m);
   }
-  if (mod) {
-    v = invariants_moderate(m);
-    if (MODE != kInv) L = from_invariants_moderate(m, v, T.at_c, T.at_t, T.sc);
-  } else {
-    v = invariants(m);
-    if (MODE != kInv) L = from_invariants(m, v, T.at_c, T.at_t, T.sc);
+  v = mod ? invariants_moderate(m) : invariants(m);
+  if (MODE == kSym && bad) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    v.i1 = v.j2 = v.j3 = v.disc = qnan;
   }
   if (MODE == kEig && WANT_FLAGS && v.disc < 0.0) f = kPending;
+  c = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
 }
 
-// Persistent fused kernel.  Work unit = a chunk of 32 consecutive records, one
-// per lane.  Every warp runs its own pipeline: lane 0 streams the warp's
-// chunks HBM -> SMEM with cp.async.bulk into a kStages-deep per-warp ring
-// completed on per-warp mbarriers, so there is no block-wide barrier in the
-// loop and warps drift into different phases (invariants vs transcendentals),
-// which is what keeps the FP64 pipe fed.  Outputs go straight from registers
-// to HBM (a warp's stores cover one contiguous 768-B lambda run).
+// Stage 2 (eigenvalues) of a record from its carry, general form.
+__device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const Tabs& T) {
+  if (bad) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    return Lam{qnan, qnan, qnan};
+  }
+  if (mod) return eig_moderate_bl(c, T.at_c, T.at_t, T.sc);
+  const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
+  return from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.at_c, T.at_t, T.sc);
+}
+
+// Per-warp record pipeline.  Work unit = a chunk of 32 consecutive records,
+// one per lane.  Lane 0 streams the warp's chunks HBM -> SMEM with
+// cp.async.bulk into a kStages-deep per-warp ring completed on per-warp
+// mbarriers: no block-wide barrier in the loop.
+struct WarpRing {
+  double* ring;
+  unsigned long long* bars;
+  const double* a;
+  long long n, nchunks, full, W;
+  int lane;
+};
+
+template <bool TMA>
+__device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
+  if (TMA && R.lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const long long c = gw + (long long)s * R.W;
+      if (c < R.full) {
+        mbar_expect_tx(&R.bars[s], kChunkBytes);
+        bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+      }
+    }
+  }
+}
+
+// Fetch chunk c (iteration it) into m[9] for this lane; returns the record count.
+template <bool TMA>
+__device__ __forceinline__ int ring_fetch(const WarpRing& R, long long c, int it, double m[9],
+                                          bool& mod) {
+  const int stage = it % kStages;
+  double* buf = R.ring + stage * (kChunk * 9);
+  const long long base = c * kChunk;
+  const int cnt = (int)min((long long)kChunk, R.n - base);
+  if (TMA && c < R.full) {
+    mbar_wait(&R.bars[stage], (uint32_t)((it / kStages) & 1));
+  } else {
+    // coalesced cooperative load: misaligned input, or the ragged last chunk
+    const double* src = R.a + base * 9;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const int e = R.lane + 32 * j;
+      buf[e] = e < cnt * 9 ? __ldg(src + e) : 1.0;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < 9; ++j) m[j] = buf[R.lane * 9 + j];
+  mod = is_moderate(m);  // consumes all nine loads before the stage is recycled
+  __syncwarp();
+  if (TMA && R.lane == 0) {
+    const long long nc = c + (long long)kStages * R.W;
+    if (nc < R.full) {
+      mbar_expect_tx(&R.bars[stage], kChunkBytes);
+      bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
+    }
+  }
+  return cnt;
+}
+
+// Persistent fused kernel, software-pipelined across records: iteration i
+// computes the invariants of chunk i and the eigenvalue stage of chunk i-1 in
+// one basic block (both branch-free in the moderate case), so the long serial
+// transcendental chain of one record overlaps the wide invariant DAG of the
+// next.  Outputs go straight from registers to HBM (a warp's lambda stores
+// cover one contiguous 768-B run; L2 merges the sectors).
 template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
@@ -150,75 +218,33 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long nchunks = (n + kChunk - 1) / kChunk;
-  const long long full = n / kChunk;
   const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const long long W = (long long)gridDim.x * kWarps;
-  double* ring = S.in[warp][0];
-  unsigned long long* bars = S.bar[warp];
+  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
+             (long long)gridDim.x * kWarps, lane};
 
   if (TMA && lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_tables(S.tab);
   __syncthreads();  // tables + barrier init; the only block-wide barrier
   const Tabs T{S.tab, S.tab + EIG33_AT_N, S.tab + 9 * EIG33_AT_N};
+  ring_prologue<TMA>(R, gw);
+  if (gw >= R.nchunks) return;
 
-  if (TMA && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const long long c = gw + (long long)s * W;
-      if (c < full) {
-        mbar_expect_tx(&bars[s], kChunkBytes);
-        bulk_load(ring + s * (kChunk * 9), a + c * (kChunk * 9), kChunkBytes, &bars[s]);
-      }
-    }
-  }
-
-  int it = 0;
-  for (long long c = gw; c < nchunks; c += W, ++it) {
-    const int stage = it % kStages;
-    double* buf = ring + stage * (kChunk * 9);
-    const long long base = c * kChunk;
-    const int cnt = (int)min((long long)kChunk, n - base);
-    if (TMA && c < full) {
-      mbar_wait(&bars[stage], (uint32_t)((it / kStages) & 1));
-    } else {
-      // coalesced cooperative load: misaligned input, or the ragged last chunk
-      const double* src = a + base * 9;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const int e = lane + 32 * j;
-        if (e < cnt * 9) buf[e] = __ldg(src + e);
-      }
-      __syncwarp();
-    }
-    double m[9];
-#pragma unroll
-    for (int j = 0; j < 9; ++j) m[j] = buf[lane * 9 + j];
-    // consume all nine loads before the stage is handed back to the TMA engine
-    const bool mod = is_moderate(m);
-    __syncwarp();
-    if (TMA && lane == 0) {
-      const long long nc = c + (long long)kStages * W;
-      if (nc < full) {
-        mbar_expect_tx(&bars[stage], kChunkBytes);
-        bulk_load(buf, a + nc * (kChunk * 9), kChunkBytes, &bars[stage]);
-      }
-    }
-    if (lane >= cnt) continue;  // ragged tail (last chunk only)
-
-    Inv v;
-    Lam L;
-    uint8_t f;
-    record<MODE, WANT_FLAGS>(m, mod, T, v, L, f);
-
-    const long long r = base + lane;
-    if (MODE != kInv) {
-      lam[r * 3 + 0] = L.l1;
-      lam[r * 3 + 1] = L.l2;
-      lam[r * 3 + 2] = L.l3;
-    }
+  // ---- prologue: stage 1 of the first chunk ----
+  double m[9];
+  bool mod, bad, pmod, pbad;
+  Inv v;
+  Carry pc;
+  uint8_t f;
+  int cnt = ring_fetch<TMA>(R, gw, 0, m, mod);
+  stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
+  pmod = mod;
+  long long pr = gw * kChunk + lane;  // record index of the carried stage
+  bool pvalid = lane < cnt;
+  auto store_stage1 = [&](long long r, bool valid) {
+    if (!valid) return;
     if (WANT_INV) {
       inv[r * 4 + 0] = v.i1;
       inv[r * 4 + 1] = v.j2;
@@ -226,6 +252,74 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       inv[r * 4 + 3] = v.disc;
     }
     if (MODE != kInv && WANT_FLAGS) flags[r] = f;
+  };
+  auto store_lam = [&](const Lam& L) {
+    if (!pvalid) return;
+    lam[pr * 3 + 0] = L.l1;
+    lam[pr * 3 + 1] = L.l2;
+    lam[pr * 3 + 2] = L.l3;
+  };
+  store_stage1(pr, pvalid);
+
+  int it = 1;
+  for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
+    cnt = ring_fetch<TMA>(R, c, it, m, mod);
+    const long long r = c * kChunk + lane;
+    const bool valid = lane < cnt;
+    Carry nc;
+    Lam L;
+    if (MODE != kSym && mod && pmod) {
+      // steady state: one branch-free block (stage 1 of r, stage 2 of pr)
+      v = invariants_moderate(m);
+      if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
+      nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+      L = eig_moderate_bl(pc, T.at_c, T.at_t, T.sc);
+      bad = false;
+    } else {
+      L = stage2(pc, pmod, pbad, T);
+      stage1<MODE, WANT_FLAGS>(m, mod, v, nc, f, bad);
+    }
+    store_lam(L);
+    store_stage1(r, valid);
+    pc = nc;
+    pmod = mod;
+    pbad = bad;
+    pr = r;
+    pvalid = valid;
+  }
+  store_lam(stage2(pc, pmod, pbad, T));
+}
+
+// Invariants-only kernel: stage 1 alone, same per-warp TMA ring.
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_invariants(const double* __restrict__ a, long long n, double* __restrict__ inv,
+                 double* /*lam: unused*/, uint8_t* /*flags: unused*/) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
+             (long long)gridDim.x * kWarps, lane};
+  if (TMA && lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  ring_prologue<TMA>(R, gw);
+  int it = 0;
+  for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
+    double m[9];
+    bool mod;
+    const int cnt = ring_fetch<TMA>(R, c, it, m, mod);
+    const Inv v = mod ? invariants_moderate(m) : invariants(m);
+    if (lane < cnt) {
+      const long long r = c * kChunk + lane;
+      inv[r * 4 + 0] = v.i1;
+      inv[r * 4 + 1] = v.j2;
+      inv[r * 4 + 2] = v.j3;
+      inv[r * 4 + 3] = v.disc;
+    }
   }
 }
 
@@ -305,7 +399,7 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
   DevInfo& d = g_dev[dev];
   const size_t smem = sizeof(Smem);
-  auto kern = k_fused<MODE, TMA, WI, WF>;
+  auto kern = MODE == kInv ? k_invariants<TMA> : k_fused<MODE, TMA, WI, WF>;
   int& occ = d.occ[MODE][TMA][WI][WF];
   if (!occ) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

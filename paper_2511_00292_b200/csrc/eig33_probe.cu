@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 namespace {
+template <int OP>
 __global__ void __launch_bounds__(256) k_dfma_rate(int iters, double seed, double* out) {
   double x[8];
 #pragma unroll
@@ -16,7 +17,12 @@ __global__ void __launch_bounds__(256) k_dfma_rate(int iters, double seed, doubl
   const double m = 0.9999999999, c = 1e-12;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], m, c);
+    for (int k = 0; k < 8; ++k) {
+      if (OP == 0) x[k] = __fma_rn(x[k], m, c);
+      if (OP == 1) x[k] = __dmul_rn(x[k], m);
+      if (OP == 2) x[k] = __dadd_rn(x[k], c);
+      if (OP == 3) x[k] = (k & 1) ? __dmul_rn(x[k], m) : __dadd_rn(x[k], c);
+    }
   }
   double s = 0;
 #pragma unroll
@@ -27,19 +33,32 @@ __global__ void __launch_bounds__(256) k_dfma_rate(int iters, double seed, doubl
 
 // Returns DFMA warp-instructions*32 (thread-level FP64 instructions) per
 // second measured over `reps` launches, or a negative value on error.
-extern "C" double eig33_probe_fp64_rate(int reps) {
+template <int OP>
+static double probe(int reps, int iters);
+extern "C" double eig33_probe_fp64_rate(int reps) { return probe<0>(reps, 4096); }
+// op: 0 DFMA, 1 DMUL, 2 DADD, 3 DMUL/DADD mix; iters scales the duration
+extern "C" double eig33_probe_fp64_op(int op, int reps, int iters) {
+  switch (op) {
+    case 1: return probe<1>(reps, iters);
+    case 2: return probe<2>(reps, iters);
+    case 3: return probe<3>(reps, iters);
+    default: return probe<0>(reps, iters);
+  }
+}
+template <int OP>
+static double probe(int reps, int iters) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   double* out = nullptr;
   if (cudaMalloc(&out, sizeof(double) * 65536) != cudaSuccess) return -1.0;
-  const int blocks = sms * 8, threads = 256, iters = 4096;
+  const int blocks = sms * 8, threads = 256;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_dfma_rate<<<blocks, threads>>>(iters, 1.0, out);  // warm-up
+  k_dfma_rate<OP><<<blocks, threads>>>(iters, 1.0, out);  // warm-up
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) k_dfma_rate<<<blocks, threads>>>(iters, 1.0 + r, out);
+  for (int r = 0; r < reps; ++r) k_dfma_rate<OP><<<blocks, threads>>>(iters, 1.0 + r, out);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -50,4 +69,59 @@ extern "C" double eig33_probe_fp64_rate(int reps) {
   if (cudaGetLastError() != cudaSuccess || ms <= 0) return -2.0;
   const double instr = (double)reps * blocks * threads * (double)iters * 8.0;
   return instr / (ms * 1e-3);
+}
+
+// Latency/ILP probe: one block of `warps` warps on one SM, each thread runs
+// `chains` independent dependent-DFMA (or DMUL / DADD) chains; returns cycles
+// per chain step measured with clock64 on warp 0.
+namespace {
+template <int CH, int OP>
+__global__ void k_lat(int iters, double* out, long long* cyc) {
+  double x[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) x[k] = 1.0 + threadIdx.x * 1e-9 + k;
+  const double m = 0.9999999999, c = 1e-12;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      if (OP == 0) x[k] = __fma_rn(x[k], m, c);
+      if (OP == 1) x[k] = __dmul_rn(x[k], m);
+      if (OP == 2) x[k] = __dadd_rn(x[k], c);
+    }
+  }
+  const long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+template <int CH, int OP>
+double lat_run(int warps) {
+  double* out;
+  long long* cyc;
+  cudaMalloc(&out, 64);
+  cudaMalloc(&cyc, 64);
+  const int iters = 4096;
+  k_lat<CH, OP><<<1, warps * 32>>>(iters, out, cyc);
+  k_lat<CH, OP><<<1, warps * 32>>>(iters, out, cyc);
+  long long h = 0;
+  cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+  cudaFree(out);
+  cudaFree(cyc);
+  return (double)h / iters;
+}
+}  // namespace
+// cycles per iteration (each iteration = `chains` FP64 ops per thread)
+extern "C" double eig33_probe_fp64_latency(int op, int chains, int warps) {
+  if (op == 0) {
+    if (chains == 1) return lat_run<1, 0>(warps);
+    if (chains == 2) return lat_run<2, 0>(warps);
+    if (chains == 4) return lat_run<4, 0>(warps);
+    return lat_run<8, 0>(warps);
+  }
+  if (op == 1) return chains == 1 ? lat_run<1, 1>(warps) : lat_run<4, 1>(warps);
+  return chains == 1 ? lat_run<1, 2>(warps) : lat_run<4, 2>(warps);
 }

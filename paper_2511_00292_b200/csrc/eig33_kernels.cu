@@ -46,7 +46,7 @@ constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth
 #define EIG33_MIN_BLOCKS 2
 #endif
 constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
-constexpr int kTabDoubles = EIG33_AT_N + 4 * EIG33_AT_N * 2 + EIG33_SC_N * 5;  // 243
+constexpr int kTabDoubles = EIG33_TAB_N;  // 225
 constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);                  // 2304
 constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
 
@@ -54,7 +54,7 @@ enum Mode { kEig = 0, kInv = 1, kSym = 2 };
 
 struct __align__(16) Smem {
   double in[kWarps][kStages][kChunk * 9];
-  double tab[kTabDoubles + 1];
+  double tab[kTabDoubles + 7];
   unsigned long long bar[kWarps][kStages];
 };
 
@@ -91,20 +91,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 __device__ __forceinline__ void load_tables(double* tab) {
-  for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) {
-    double v;
-    if (i < EIG33_AT_N)
-      v = eig33_at_c[i];
-    else if (i < EIG33_AT_N + 8 * EIG33_AT_N)
-      v = eig33_at_t[i - EIG33_AT_N];
-    else
-      v = eig33_sc[i - 9 * EIG33_AT_N];
-    tab[i] = v;
-  }
+  for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) tab[i] = eig33_tab[i];
 }
 
 struct Tabs {
-  const double *at_c, *at_t, *sc;
+  const double* tab;
 };
 
 // Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
@@ -141,9 +132,9 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     return Lam{qnan, qnan, qnan};
   }
-  if (mod) return eig_moderate_bl(c, T.at_c, T.at_t, T.sc);
+  if (mod) return eig_moderate_bl(c, T.tab);
   const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
-  return from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.at_c, T.at_t, T.sc);
+  return from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
 }
 
 // Per-warp record pipeline.  Work unit = a chunk of 32 consecutive records,
@@ -228,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
   load_tables(S.tab);
   __syncthreads();  // tables + barrier init; the only block-wide barrier
-  const Tabs T{S.tab, S.tab + EIG33_AT_N, S.tab + 9 * EIG33_AT_N};
+  const Tabs T{S.tab};
   ring_prologue<TMA>(R, gw);
   if (gw >= R.nchunks) return;
 
@@ -241,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   int cnt = ring_fetch<TMA>(R, gw, 0, m, mod);
   stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
   pmod = mod;
+  bool pfast = mod && fast_carry(v);
   long long pr = gw * kChunk + lane;  // record index of the carried stage
   bool pvalid = lane < cnt;
   auto store_stage1 = [&](long long r, bool valid) {
@@ -268,12 +260,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const bool valid = lane < cnt;
     Carry nc;
     Lam L;
-    if (MODE != kSym && mod && pmod) {
-      // steady state: one branch-free block (stage 1 of r, stage 2 of pr)
+    if (MODE != kSym && mod && pfast) {
+      // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
+      // the long transcendental chain is written first so the scheduler
+      // starts it early and fills its latency with the invariant DAG.
+#if EIG33_EIG_FIRST
+      L = eig_fast(pc, T.tab);
       v = invariants_moderate(m);
+#else
+      v = invariants_moderate(m);
+      L = eig_fast(pc, T.tab);
+#endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
-      L = eig_moderate_bl(pc, T.at_c, T.at_t, T.sc);
       bad = false;
     } else {
       L = stage2(pc, pmod, pbad, T);
@@ -283,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     store_stage1(r, valid);
     pc = nc;
     pmod = mod;
+    pfast = mod && fast_carry(v);
     pbad = bad;
     pr = r;
     pvalid = valid;
@@ -361,12 +361,12 @@ __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict_
 __global__ void __launch_bounds__(kThreads) k_triple_angle(const double* __restrict__ j3,
                                                            const double* __restrict__ disc,
                                                            long long n, double* __restrict__ phi) {
-  __shared__ double tab[kTabDoubles + 1];
+  __shared__ __align__(16) double tab[kTabDoubles + 7];
   load_tables(tab);
   __syncthreads();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    phi[i] = triple_angle(j3[i], disc[i], tab, tab + EIG33_AT_N);
+    phi[i] = triple_angle(j3[i], disc[i], tab);
 }
 
 // ---------------------------------------------------------------------------

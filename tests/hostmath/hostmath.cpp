@@ -19,10 +19,26 @@ static Inv inv_path(const double* m, int path) {
 }
 static Lam lam_path(const double* m, const Inv& v, int path) {
   if (path == 2 || (path == 0 && is_moderate(m)))
-    return from_invariants_moderate(m, v, eig33_at_c, eig33_at_t, eig33_sc);
-  return from_invariants(m, v, eig33_at_c, eig33_at_t, eig33_sc);
+    return from_invariants_moderate(m, v, eig33_tab);
+  return from_invariants(m, v, eig33_tab);
 }
 int hm_is_moderate(const double* a) { return is_moderate(a) ? 1 : 0; }
+// path 3: the kernel's steady-state block (eig_fast) where its preconditions
+// hold (moderate, j2 > 0, disc > 0), else path 0
+void hm_eigvals_fast(const double* a, size_t n, double* lam) {
+  for (size_t i = 0; i < n; ++i) {
+    const double* m = a + 9 * i;
+    Lam l;
+    if (is_moderate(m)) {
+      const Inv v = invariants_moderate(m);
+      const Carry c{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+      l = fast_carry(v) ? eig_fast(c, eig33_tab) : eig_moderate_bl(c, eig33_tab);
+    } else {
+      l = from_invariants(m, invariants(m), eig33_tab);
+    }
+    lam[3 * i] = l.l1; lam[3 * i + 1] = l.l2; lam[3 * i + 2] = l.l3;
+  }
+}
 void hm_invariants_path(const double* a, size_t n, double* inv, int path) {
   for (size_t i = 0; i < n; ++i) {
     const Inv v = inv_path(a + 9 * i, path);
@@ -51,13 +67,13 @@ void hm_eigvals(const double* a, size_t n, double* lam, uint8_t* adv) {
   }
 }
 void hm_atan2(const double* y, const double* x, size_t n, double* out) {
-  for (size_t i = 0; i < n; ++i) out[i] = atan2_pos(y[i], x[i], eig33_at_c, eig33_at_t);
+  for (size_t i = 0; i < n; ++i) out[i] = atan2_pos(y[i], x[i], eig33_tab);
 }
 void hm_triple_angle(const double* j3, const double* disc, size_t n, double* out) {
-  for (size_t i = 0; i < n; ++i) out[i] = triple_angle(j3[i], disc[i], eig33_at_c, eig33_at_t);
+  for (size_t i = 0; i < n; ++i) out[i] = triple_angle(j3[i], disc[i], eig33_tab);
 }
 void hm_sincos(const double* th, size_t n, double* s, double* c) {
-  for (size_t i = 0; i < n; ++i) sincos_small(th[i], eig33_sc, s + i, c + i);
+  for (size_t i = 0; i < n; ++i) sincos_small(th[i], eig33_tab, s + i, c + i);
 }
 void hm_div(const double* x, size_t n, int which, double* out) {
   for (size_t i = 0; i < n; ++i) out[i] = which == 3 ? div3(x[i]) : which == 6 ? div6(x[i]) : div27(x[i]);

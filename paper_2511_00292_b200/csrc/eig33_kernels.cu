@@ -39,9 +39,10 @@ constexpr int kThreads = EIG33_THREADS;  // threads per block
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 32;     // records per warp chunk (one per lane)
 #ifndef EIG33_STAGES
-#define EIG33_STAGES 3
+#define EIG33_STAGES 4
 #endif
-constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth
+constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth (power of two)
+static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
 #ifndef EIG33_MIN_BLOCKS
 #define EIG33_MIN_BLOCKS 2
 #endif
@@ -164,16 +165,18 @@ __device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
 
 // Fetch chunk c (iteration it) into m[9] for this lane; returns the record count.
 template <bool TMA>
-__device__ __forceinline__ int ring_fetch(const WarpRing& R, long long c, int it, double m[9],
+__device__ __forceinline__ int ring_fetch(const WarpRing& R, long long c, uint32_t it, double m[9],
                                           bool& mod) {
-  const int stage = it % kStages;
+  const uint32_t stage = it & (kStages - 1);
   double* buf = R.ring + stage * (kChunk * 9);
-  const long long base = c * kChunk;
-  const int cnt = (int)min((long long)kChunk, R.n - base);
-  if (TMA && c < R.full) {
-    mbar_wait(&R.bars[stage], (uint32_t)((it / kStages) & 1));
+  const bool full_chunk = c < R.full;
+  int cnt = kChunk;
+  if (TMA && full_chunk) {
+    mbar_wait(&R.bars[stage], (it / kStages) & 1u);
   } else {
     // coalesced cooperative load: misaligned input, or the ragged last chunk
+    const long long base = c * kChunk;
+    cnt = (int)min((long long)kChunk, R.n - base);
     const double* src = R.a + base * 9;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   };
   store_stage1(pr, pvalid);
 
-  int it = 1;
+  uint32_t it = 1;
   for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
     cnt = ring_fetch<TMA>(R, c, it, m, mod);
     const long long r = c * kChunk + lane;
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
   __syncthreads();
   ring_prologue<TMA>(R, gw);
-  int it = 0;
+  uint32_t it = 0;
   for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
     double m[9];
     bool mod;

@@ -47,7 +47,7 @@ static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
 #define EIG33_MIN_BLOCKS 2
 #endif
 constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
-constexpr int kTabDoubles = EIG33_TAB_N;  // 225
+constexpr int kTabDoubles = EIG33_TAB_N;
 constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);                  // 2304
 constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
 

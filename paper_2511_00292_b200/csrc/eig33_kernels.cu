@@ -37,9 +37,14 @@ namespace eig33b {
 #endif
 constexpr int kThreads = EIG33_THREADS;  // threads per block
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 32;     // records per warp chunk (one per lane)
+#ifndef EIG33_RPL
+#define EIG33_RPL 2
+#endif
+constexpr int kRPL = EIG33_RPL;  // records per lane per chunk (1 or 2)
+static_assert(kRPL == 1 || kRPL == 2, "kRPL must be 1 or 2");
+constexpr int kChunk = 32 * kRPL;  // records per warp chunk
 #ifndef EIG33_STAGES
-#define EIG33_STAGES 4
+#define EIG33_STAGES (4 / EIG33_RPL)
 #endif
 constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth (power of two)
 static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
@@ -48,7 +53,7 @@ static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
 #endif
 constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
 constexpr int kTabDoubles = EIG33_TAB_N;
-constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);                  // 2304
+constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);  // 2304 * kRPL
 constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
 
 enum Mode { kEig = 0, kInv = 1, kSym = 2 };
@@ -163,40 +168,51 @@ __device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
   }
 }
 
-// Fetch chunk c (iteration it) into m[9] for this lane; returns the record count.
+// Chunk c (iteration it) of this warp: wait for its TMA (or load it
+// cooperatively: misaligned input / ragged last chunk); returns the SMEM
+// buffer and the record count.
 template <bool TMA>
-__device__ __forceinline__ int ring_fetch(const WarpRing& R, long long c, uint32_t it, double m[9],
-                                          bool& mod) {
+__device__ __forceinline__ double* ring_acquire(const WarpRing& R, long long c, uint32_t it,
+                                                int& cnt) {
   const uint32_t stage = it & (kStages - 1);
   double* buf = R.ring + stage * (kChunk * 9);
-  const bool full_chunk = c < R.full;
-  int cnt = kChunk;
-  if (TMA && full_chunk) {
+  cnt = kChunk;
+  if (TMA && c < R.full) {
     mbar_wait(&R.bars[stage], (it / kStages) & 1u);
   } else {
-    // coalesced cooperative load: misaligned input, or the ragged last chunk
     const long long base = c * kChunk;
     cnt = (int)min((long long)kChunk, R.n - base);
     const double* src = R.a + base * 9;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
+    for (int j = 0; j < 9 * kRPL; ++j) {
       const int e = R.lane + 32 * j;
       buf[e] = e < cnt * 9 ? __ldg(src + e) : 1.0;
     }
     __syncwarp();
   }
+  return buf;
+}
+// Record h (0..kRPL-1) of this lane from the chunk buffer; `mod` consumes all
+// nine loads, so once every record of the chunk is read the stage can be
+// handed back to the TMA engine (ring_release).
+__device__ __forceinline__ void ring_read(const double* buf, int lane, int h, double m[9],
+                                          bool& mod) {
 #pragma unroll
-  for (int j = 0; j < 9; ++j) m[j] = buf[R.lane * 9 + j];
-  mod = is_moderate(m);  // consumes all nine loads before the stage is recycled
+  for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
+  mod = is_moderate(m);
+}
+template <bool TMA>
+__device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
+                                             double* buf) {
   __syncwarp();
   if (TMA && R.lane == 0) {
+    const uint32_t stage = it & (kStages - 1);
     const long long nc = c + (long long)kStages * R.W;
     if (nc < R.full) {
       mbar_expect_tx(&R.bars[stage], kChunkBytes);
       bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
     }
   }
-  return cnt;
 }
 
 // Persistent fused kernel, software-pipelined across records: iteration i
@@ -226,18 +242,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   ring_prologue<TMA>(R, gw);
   if (gw >= R.nchunks) return;
 
-  // ---- prologue: stage 1 of the first chunk ----
   double m[9];
-  bool mod, bad, pmod, pbad;
+  bool mod, bad, pmod, pbad, pfast, pvalid;
   Inv v;
   Carry pc;
   uint8_t f;
-  int cnt = ring_fetch<TMA>(R, gw, 0, m, mod);
-  stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
-  pmod = mod;
-  bool pfast = mod && fast_carry(v);
-  long long pr = gw * kChunk + lane;  // record index of the carried stage
-  bool pvalid = lane < cnt;
+  long long pr;  // record index of the carried stage
   auto store_stage1 = [&](long long r, bool valid) {
     if (!valid) return;
     if (WANT_INV) {
@@ -254,13 +264,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     lam[pr * 3 + 1] = L.l2;
     lam[pr * 3 + 2] = L.l3;
   };
-  store_stage1(pr, pvalid);
-
-  uint32_t it = 1;
-  for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
-    cnt = ring_fetch<TMA>(R, c, it, m, mod);
-    const long long r = c * kChunk + lane;
-    const bool valid = lane < cnt;
+  // One step of the record pipeline: stage 2 of the carried record, stage 1 of m.
+  auto step = [&](long long r, bool valid) {
     Carry nc;
     Lam L;
     if (MODE != kSym && mod && pfast) {
@@ -289,6 +294,37 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     pbad = bad;
     pr = r;
     pvalid = valid;
+  };
+
+  // ---- prologue: first chunk; stage 1 of its first record ----
+  int cnt;
+  double* buf = ring_acquire<TMA>(R, gw, 0, cnt);
+  ring_read(buf, lane, 0, m, mod);
+  if (kRPL == 1) ring_release<TMA>(R, gw, 0, buf);
+  stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
+  pmod = mod;
+  pfast = mod && fast_carry(v);
+  pr = gw * kChunk + lane;
+  pvalid = lane < cnt;
+  store_stage1(pr, pvalid);
+  if (kRPL == 2) {
+    ring_read(buf, lane, 1, m, mod);
+    ring_release<TMA>(R, gw, 0, buf);
+    step(gw * kChunk + 32 + lane, 32 + lane < cnt);
+  }
+
+  uint32_t it = 1;
+  for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
+    buf = ring_acquire<TMA>(R, c, it, cnt);
+    const long long base = c * kChunk + lane;
+    ring_read(buf, lane, 0, m, mod);
+    if (kRPL == 1) ring_release<TMA>(R, c, it, buf);
+    step(base, lane < cnt);
+    if (kRPL == 2) {
+      ring_read(buf, lane, 1, m, mod);
+      ring_release<TMA>(R, c, it, buf);
+      step(base + 32, 32 + lane < cnt);
+    }
   }
   store_lam(stage2(pc, pmod, pbad, T));
 }
@@ -312,16 +348,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   ring_prologue<TMA>(R, gw);
   uint32_t it = 0;
   for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
-    double m[9];
-    bool mod;
-    const int cnt = ring_fetch<TMA>(R, c, it, m, mod);
-    const Inv v = mod ? invariants_moderate(m) : invariants(m);
-    if (lane < cnt) {
-      const long long r = c * kChunk + lane;
-      inv[r * 4 + 0] = v.i1;
-      inv[r * 4 + 1] = v.j2;
-      inv[r * 4 + 2] = v.j3;
-      inv[r * 4 + 3] = v.disc;
+    int cnt;
+    double* buf = ring_acquire<TMA>(R, c, it, cnt);
+#pragma unroll
+    for (int h = 0; h < kRPL; ++h) {
+      double m[9];
+      bool mod;
+      ring_read(buf, lane, h, m, mod);
+      if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
+      const Inv v = mod ? invariants_moderate(m) : invariants(m);
+      if (lane + 32 * h < cnt) {
+        const long long r = c * kChunk + 32 * h + lane;
+        inv[r * 4 + 0] = v.i1;
+        inv[r * 4 + 1] = v.j2;
+        inv[r * 4 + 2] = v.j3;
+        inv[r * 4 + 3] = v.disc;
+      }
     }
   }
 }
@@ -416,7 +458,8 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
     }
     occ = o > 0 ? o : 1;
   }
-  const long long nblk = (long long)((n + kThreads - 1) / kThreads);  // one chunk per warp
+  const long long nchunks = (long long)((n + kChunk - 1) / kChunk);
+  const long long nblk = (nchunks + kWarps - 1) / kWarps;  // at least one chunk per warp
   const long long cap = (long long)d.sms * occ;
   const long long grid = nblk < cap ? nblk : cap;
   kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);

@@ -66,6 +66,20 @@ int eig33cu_eigvalss(const double* d_a, size_t n, double* d_inv, double* d_lam,
 int eig33cu_triple_angle(const double* d_j3, const double* d_disc, size_t n, double* d_phi,
                          void* stream);
 
+/* Accuracy-study variants (not on the throughput path), bit-exact like the rest:
+ *  - eig33::invariants(a, v) for v = 0 Stable, 1 Naive, 2 NaiveTensor
+ *    (reference include/eig33/invariants.hpp:74, src/invariants.cpp:76-98);
+ *  - eig33::eigvals_naive (include/eig33/eigensolver.hpp:49, src/eigensolver.cpp:119-123),
+ *    flags bit0 = non_real_advisory;
+ *  - eig33::jacobian_j2 / jacobian_j3 / jacobian_disc (include/eig33/invariants.hpp:62-69,
+ *    src/invariants.cpp:60-74): n x 9 row-major gradients, any output may be NULL. */
+int eig33cu_invariants_variant(const double* d_a, size_t n, int variant, double* d_inv,
+                               void* stream);
+int eig33cu_eigvals_naive(const double* d_a, size_t n, double* d_lam, uint8_t* d_flags,
+                          void* stream);
+int eig33cu_jacobians(const double* d_a, size_t n, double* d_jj2, double* d_jj3, double* d_jdisc,
+                      void* stream);
+
 /* Synchronous host-buffer versions on one device (chunked, pipelined
  * H2D / kernel / D2H over 3 streams).  eig33_eigvalss_host returns
  * EIG33_ENOTSYM if any matrix failed the symmetry gate (outputs still written). */

@@ -314,3 +314,115 @@ int orc_eigvals_mt(const double *a, size_t n, double *inv, double *lam, int nthr
   for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
   return 0;
 }
+
+/* ---- accuracy-study variants ---- */
+
+/* src/invariants.cpp:21-28 */
+static double orc_j2_naive(const double *m) {
+  const double a00 = m[0], a01 = m[1], a02 = m[2], a10 = m[3], a11 = m[4], a12 = m[5];
+  const double a20 = m[6], a21 = m[7], a22 = m[8];
+  return (a00 * a00 - a00 * a11 - a00 * a22 + 3.0 * a01 * a10 + 3.0 * a02 * a20 + a11 * a11 -
+          a11 * a22 + 3.0 * a12 * a21 + a22 * a22) /
+         3.0;
+}
+
+/* src/invariants.cpp:38-52 */
+static double orc_j3_naive(const double *m) {
+  const double a00 = m[0], a01 = m[1], a02 = m[2], a10 = m[3], a11 = m[4], a12 = m[5];
+  const double a20 = m[6], a21 = m[7], a22 = m[8];
+  double s = 2.0 * a00 * a00 * a00;
+  s -= 3.0 * a00 * a00 * a11;
+  s -= 3.0 * a00 * a00 * a22;
+  s += 9.0 * a00 * a01 * a10;
+  s += 9.0 * a00 * a02 * a20;
+  s -= 3.0 * a00 * a11 * a11;
+  s += 12.0 * a00 * a11 * a22;
+  s -= 18.0 * a00 * a12 * a21;
+  s -= 3.0 * a00 * a22 * a22;
+  s += 9.0 * a01 * a10 * a11;
+  s -= 18.0 * a01 * a10 * a22;
+  s += 27.0 * a01 * a12 * a20;
+  s += 27.0 * a02 * a10 * a21;
+  s -= 18.0 * a02 * a11 * a20;
+  s += 9.0 * a02 * a20 * a22;
+  s += 2.0 * a11 * a11 * a11;
+  s -= 3.0 * a11 * a11 * a22;
+  s += 9.0 * a11 * a12 * a21;
+  s -= 3.0 * a11 * a22 * a22;
+  s += 9.0 * a12 * a21 * a22;
+  s += 2.0 * a22 * a22 * a22;
+  return s / 27.0;
+}
+
+/* src/invariants.cpp:30-34 with matmul/trace, src/mat3.cpp:7,18-26 */
+static double orc_j2_tensor(const double *m) {
+  double d[9];
+  orc_dev(m, d);
+  double t[3];
+  for (int i = 0; i < 3; ++i)
+    t[i] = d[3 * i] * d[i] + d[3 * i + 1] * d[3 + i] + d[3 * i + 2] * d[6 + i];
+  return (t[0] + t[1] + t[2]) / 2.0;
+}
+
+/* src/invariants.cpp:54 with det, src/mat3.cpp:49-55 */
+static double orc_j3_tensor(const double *m) {
+  double d[9];
+  orc_dev(m, d);
+  return d[0] * (d[4] * d[8] - d[5] * d[7]) - d[1] * (d[3] * d[8] - d[5] * d[6]) +
+         d[2] * (d[3] * d[7] - d[4] * d[6]);
+}
+
+/* src/invariants.cpp:58 */
+static double orc_disc_naive(double j2, double j3) { return 4.0 * j2 * j2 * j2 - 27.0 * j3 * j3; }
+
+/* invariants(a, v), src/invariants.cpp:76-98: v = 0 Stable, 1 Naive, 2 NaiveTensor */
+void orc_invariants_variant(const double *a, size_t n, int v, double *inv) {
+  if (v == 0) {
+    orc_invariants(a, n, inv);
+    return;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const double *m = a + 9 * i;
+    const double j2 = v == 1 ? orc_j2_naive(m) : orc_j2_tensor(m);
+    const double j3 = v == 1 ? orc_j3_naive(m) : orc_j3_tensor(m);
+    inv[4 * i + 0] = orc_i1(m);
+    inv[4 * i + 1] = j2;
+    inv[4 * i + 2] = j3;
+    inv[4 * i + 3] = orc_disc_naive(j2, j3);
+  }
+}
+
+/* eigvals_naive, src/eigensolver.cpp:119-123 */
+void orc_eigvals_naive(const double *a, size_t n, double *lam, uint8_t *adv) {
+  for (size_t i = 0; i < n; ++i) {
+    const double *m = a + 9 * i;
+    const double j2 = orc_j2_naive(m), j3 = orc_j3_naive(m);
+    orc_from_invariants(m, orc_i1(m), j2, j3, orc_disc_naive(j2, j3), lam + 3 * i,
+                        adv ? adv + i : NULL);
+  }
+}
+
+/* jacobian_j2 / j3 / disc, src/invariants.cpp:60-74; each output n x 9, nullable */
+void orc_jacobians(const double *a, size_t n, double *jj2, double *jj3, double *jdisc) {
+  for (size_t i = 0; i < n; ++i) {
+    const double *m = a + 9 * i;
+    double dv[9], cd[9], g[9];
+    orc_dev(m, dv);
+    if (jj2)
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) jj2[9 * i + 3 * r + c] = dv[3 * c + r];
+    if (jj3) {
+      orc_cofactor(dv, cd);
+      orc_dev(cd, jj3 + 9 * i);
+    }
+    if (jdisc) {
+      const orc_ddiff d = orc_diag_diff(m);
+      const double j2 = orc_j2(m, d), j3 = orc_j3(m, d);
+      const double c2 = (12.0 * j2) * j2, c3 = 54.0 * j3;
+      orc_cofactor(dv, cd);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) g[3 * r + c] = c2 * m[3 * c + r] - c3 * cd[3 * r + c];
+      orc_dev(g, jdisc + 9 * i);
+    }
+  }
+}

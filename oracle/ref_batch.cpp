@@ -104,3 +104,52 @@ std::uint64_t ref_checksum_loop(const double* a, std::uint64_t n) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// invariants(a, v) for v = 0 Stable, 1 Naive, 2 NaiveTensor (include/eig33/invariants.hpp:74)
+int ref_invariants_variant(const double* a, std::size_t n, int v, double* inv, int nthreads) {
+  const auto var = v == 0 ? eig33::AlgorithmVariant::Stable
+                   : v == 1 ? eig33::AlgorithmVariant::Naive
+                            : eig33::AlgorithmVariant::NaiveTensor;
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto s = eig33::invariants(load(a + 9 * i), var);
+      inv[4 * i + 0] = s.i1;
+      inv[4 * i + 1] = s.j2;
+      inv[4 * i + 2] = s.j3;
+      inv[4 * i + 3] = s.disc;
+    }
+  });
+  return 0;
+}
+
+// eigvals_naive (include/eig33/eigensolver.hpp:49)
+int ref_eigvals_naive(const double* a, std::size_t n, double* lam, std::uint8_t* adv, int nthreads) {
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto t = eig33::eigvals_naive(load(a + 9 * i));
+      lam[3 * i + 0] = t.lambda1;
+      lam[3 * i + 1] = t.lambda2;
+      lam[3 * i + 2] = t.lambda3;
+      if (adv) adv[i] = t.non_real_advisory ? 1 : 0;
+    }
+  });
+  return 0;
+}
+
+// jacobian_j2 / jacobian_j3 / jacobian_disc (include/eig33/invariants.hpp:62-69)
+int ref_jacobians(const double* a, std::size_t n, double* jj2, double* jj3, double* jdisc,
+                  int nthreads) {
+  parallel_shards(n, nthreads, [=](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const eig33::Mat3 m = load(a + 9 * i);
+      if (jj2) std::memcpy(jj2 + 9 * i, eig33::jacobian_j2(m).e.data(), 72);
+      if (jj3) std::memcpy(jj3 + 9 * i, eig33::jacobian_j3(m).e.data(), 72);
+      if (jdisc) std::memcpy(jdisc + 9 * i, eig33::jacobian_disc(m).e.data(), 72);
+    }
+  });
+  return 0;
+}
+
+}  // extern "C"

@@ -27,6 +27,7 @@ import numpy as np
 
 __all__ = [
     "eigvals", "eigvalss", "invariants", "triple_angle", "generate", "multi_eigvals",
+    "eigvals_naive", "jacobians", "VARIANTS",
     "lib", "EigResult", "eps_mach", "FLAG_ADVISORY", "FLAG_NOT_SYMMETRIC",
 ]
 
@@ -43,7 +44,9 @@ C_ABI_SYMBOLS = (
     "eig33cu_version", "eig33cu_last_error", "eig33cu_invariants", "eig33cu_eigvals",
     "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
     "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
+    "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
 )
+VARIANTS = {"Stable": 0, "Naive": 1, "NaiveTensor": 2}  # reference AlgorithmVariant
 
 _lib = None
 
@@ -71,6 +74,9 @@ def lib() -> ctypes.CDLL:
         "eig33_eigvalss_host": ([P, S, P, P, P, I], I),
         "eig33_multi_eigvals": ([P, S, P, P, P, I], I),
         "eig33cu_generate": ([I, U64, U64, S, P, P], I),
+        "eig33cu_invariants_variant": ([P, S, I, P, P], I),
+        "eig33cu_eigvals_naive": ([P, S, P, P, P], I),
+        "eig33cu_jacobians": ([P, S, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -212,8 +218,27 @@ def eigvalss(a, *, return_invariants=False, return_flags=False, device=0) -> Eig
                        return_invariants, return_flags, device)
 
 
-def invariants(a, *, device=0):
-    """Batched ``eig33::invariants(a, AlgorithmVariant::Stable)``: (n,4) {i1,j2,j3,disc}."""
+def _to_cuda(a, device):
+    """Host input -> (CUDA (n,9) tensor, True) for the device-only study kernels."""
+    torch = _torch()
+    if _is_cuda_tensor(a):
+        return _records_cuda(a), False
+    return torch.from_numpy(_records_np(a)).to(f"cuda:{int(device)}"), True
+
+
+def invariants(a, *, variant="Stable", device=0):
+    """Batched ``eig33::invariants(a, variant)`` (reference invariants.hpp:74):
+    (n,4) {i1,j2,j3,disc}; variant "Stable" (the hot path), "Naive" or "NaiveTensor"."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown AlgorithmVariant {variant!r}")
+    if variant != "Stable":
+        torch = _torch()
+        d, host = _to_cuda(a, device)
+        with torch.cuda.device(d.device):
+            out = torch.empty((d.shape[0], 4), dtype=torch.float64, device=d.device)
+            _check(lib().eig33cu_invariants_variant(_ptr(d), d.shape[0], VARIANTS[variant], _ptr(out),
+                                                    _stream(d)), "invariants")
+        return out.cpu().numpy() if host else out
     L = lib()
     if _is_cuda_tensor(a):
         torch = _torch()
@@ -226,6 +251,34 @@ def invariants(a, *, device=0):
     inv = np.empty((arr.shape[0], 4))
     _check(L.eig33_invariants_host(_ptr(arr), arr.shape[0], _ptr(inv), int(device)), "invariants")
     return inv
+
+
+def eigvals_naive(a, *, return_flags=False, device=0) -> EigResult:
+    """Batched ``eig33::eigvals_naive`` (reference eigensolver.hpp:49): the
+    error-study path fed by the naive invariants."""
+    torch = _torch()
+    d, host = _to_cuda(a, device)
+    with torch.cuda.device(d.device):
+        lam = torch.empty((d.shape[0], 3), dtype=torch.float64, device=d.device)
+        fl = torch.empty((d.shape[0],), dtype=torch.uint8, device=d.device) if return_flags else None
+        _check(lib().eig33cu_eigvals_naive(_ptr(d), d.shape[0], _ptr(lam), _ptr(fl), _stream(d)),
+               "eigvals_naive")
+    if host:
+        return EigResult(lam.cpu().numpy(), None, None if fl is None else fl.cpu().numpy())
+    return EigResult(lam, None, fl)
+
+
+def jacobians(a, *, device=0):
+    """Batched ``eig33::jacobian_j2 / jacobian_j3 / jacobian_disc`` (reference
+    invariants.hpp:62-69): three (n,3,3) row-major gradients."""
+    torch = _torch()
+    d, host = _to_cuda(a, device)
+    n = d.shape[0]
+    with torch.cuda.device(d.device):
+        outs = [torch.empty((n, 9), dtype=torch.float64, device=d.device) for _ in range(3)]
+        _check(lib().eig33cu_jacobians(_ptr(d), n, *(_ptr(o) for o in outs), _stream(d)), "jacobians")
+    outs = [o.view(n, 3, 3) for o in outs]
+    return tuple(o.cpu().numpy() for o in outs) if host else tuple(outs)
 
 
 def triple_angle(j3, disc):

@@ -27,7 +27,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
     "-Xptxas", "-v",
 ]
-SOURCES = ["eig33_kernels.cu", "eig33_gen.cu", "eig33_host.cpp", "eig33_probe.cu"]
+SOURCES = ["eig33_kernels.cu", "eig33_gen.cu", "eig33_aux.cu", "eig33_host.cpp", "eig33_probe.cu"]
 
 
 def _nvcc():

@@ -90,3 +90,21 @@ void hm_libm_sincos(const double* th, size_t n, double* s, double* c) {
   for (size_t i = 0; i < n; ++i) ::sincos(th[i], s + i, c + i);
 }
 }
+
+extern "C" {
+void hm_invariants_variant(const double* a, size_t n, int v, double* inv) {
+  for (size_t i = 0; i < n; ++i) {
+    const Inv s = invariants_variant(a + 9 * i, v);
+    inv[4 * i] = s.i1; inv[4 * i + 1] = s.j2; inv[4 * i + 2] = s.j3; inv[4 * i + 3] = s.disc;
+  }
+}
+void hm_jacobians(const double* a, size_t n, double* jj2, double* jj3, double* jdisc) {
+  for (size_t i = 0; i < n; ++i) {
+    const double* m = a + 9 * i;
+    jacobian_j2(m, jj2 + 9 * i);
+    jacobian_j3(m, jj3 + 9 * i);
+    const Inv s = invariants(m);
+    jacobian_disc(m, s.j2, s.j3, jdisc + 9 * i);
+  }
+}
+}

@@ -105,3 +105,20 @@ def test_product_math_parity_vs_checker():
     err = U.lam_error_units(lam, lam_r)
     assert err.max() <= U.TOL_UNITS
     assert (err == 0).mean() > 0.995
+
+
+@pytest.mark.skipif(U.ref() is None, reason="compiled reference not built")
+def test_product_study_variants_bitwise():
+    a = U.mixed_corpus(1 << 16, 29)
+    n = a.shape[0]
+    H, R = U.hostmath(), U.ref()
+    for v in (1, 2):
+        x, y = np.empty((n, 4)), np.empty((n, 4))
+        H.hm_invariants_variant(U.ptr(a), U.S(n), v, U.ptr(x))
+        R.ref_invariants_variant(U.ptr(a), U.S(n), v, U.ptr(y), U.nthreads())
+        assert U.bit_equal(x, y).all()
+    js = [np.empty((n, 9)) for _ in range(6)]
+    H.hm_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[:3]))
+    R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[3:]), U.nthreads())
+    for k in range(3):
+        assert U.bit_equal(js[k], js[k + 3]).all()

@@ -136,3 +136,26 @@ def test_eigvalss_symmetry_gate():
                   [1.0, 1.0, 0, 1.0 + 2.0 ** -52, 2, 0, 0, 0, 3]])
     _, st = _port_sym(a)
     assert list(st) == [1, 1, 0]  # test_eigensolver.cpp:150-165
+
+
+@pytest.mark.skipif(U.ref() is None, reason="compiled reference not built")
+def test_port_study_variants_bitwise_equal_compiled_reference():
+    """naive / tensor invariants, eigvals_naive, Jacobians."""
+    a = U.mixed_corpus(1 << 15, 23)
+    n = a.shape[0]
+    P, R = U.port(), U.ref()
+    for v in (1, 2):
+        x, y = np.empty((n, 4)), np.empty((n, 4))
+        P.orc_invariants_variant(U.ptr(a), U.S(n), v, U.ptr(x))
+        R.ref_invariants_variant(U.ptr(a), U.S(n), v, U.ptr(y), U.nthreads())
+        assert U.bit_equal(x, y).all()
+    l1, l2 = np.empty((n, 3)), np.empty((n, 3))
+    f1, f2 = np.empty(n, np.uint8), np.empty(n, np.uint8)
+    P.orc_eigvals_naive(U.ptr(a), U.S(n), U.ptr(l1), U.ptr(f1))
+    R.ref_eigvals_naive(U.ptr(a), U.S(n), U.ptr(l2), U.ptr(f2), U.nthreads())
+    assert U.bit_equal(l1, l2).all() and (f1 == f2).all()
+    js = [np.empty((n, 9)) for _ in range(6)]
+    P.orc_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[:3]))
+    R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[3:]), U.nthreads())
+    for k in range(3):
+        assert U.bit_equal(js[k], js[k + 3]).all()

@@ -238,3 +238,26 @@ def test_cxx_batch_api_links_and_runs(tmp_path):
     assert r.returncode == 0, r.stderr
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == "OK", out.stdout + out.stderr
+
+
+def test_study_variants_on_device():
+    """naive / tensor invariants, eigvals_naive (+advisory), Jacobians vs the
+    compiled reference: bit-exact except eigvals_naive's lambda (tolerance)."""
+    a = U.mixed_corpus(1 << 18, 31)
+    n = a.shape[0]
+    R = U.ref() or pytest.skip("compiled reference not available")
+    for name, v in (("Naive", 1), ("NaiveTensor", 2)):
+        got = eig.invariants(a, variant=name)
+        want = np.empty((n, 4))
+        R.ref_invariants_variant(U.ptr(a), U.S(n), v, U.ptr(want), U.nthreads())
+        assert U.bit_equal(got, want).all(), name
+    r = eig.eigvals_naive(a, return_flags=True)
+    lam, fl = np.empty((n, 3)), np.empty(n, np.uint8)
+    R.ref_eigvals_naive(U.ptr(a), U.S(n), U.ptr(lam), U.ptr(fl), U.nthreads())
+    assert ((r.flags & 1) == fl).all()
+    assert (U.lam_error_units(r.lam, lam) <= U.TOL_UNITS).all()
+    j2, j3, jd = eig.jacobians(a)
+    want = [np.empty((n, 9)) for _ in range(3)]
+    R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(w) for w in want), U.nthreads())
+    for got, w in zip((j2, j3, jd), want):
+        assert U.bit_equal(got.reshape(n, 9), w).all()

@@ -40,7 +40,7 @@ HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=400)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=N_PER_GPU_DEFAULT, help="records per GPU")
@@ -130,6 +130,8 @@ def cpu_eigvals_rate(a, seconds, threads):
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
+    """nvidia-smi sampler (100 ms); stats cover only the samples taken between
+    mark_start() and mark_stop(), i.e. the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -137,7 +139,8 @@ class Clocks:
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host time, csv line)
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -152,12 +155,18 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        time.sleep(0.25)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -165,7 +174,11 @@ class Clocks:
             self.proc.kill()
         sm, mx, pw, reasons = [], None, [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 or 0.0
+        t1 = self.t1 or float("inf")
+        for ts, ln in self.lines:
+            if not (t0 <= ts <= t1 + 0.1):
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -292,11 +305,13 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     e1.synchronize()
+    clocks.mark_stop()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()

@@ -268,7 +268,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   auto step = [&](long long r, bool valid) {
     Carry nc;
     Lam L;
-    if (MODE != kSym && mod && pfast) {
+    bool sym_ok = true;
+    if (MODE == kSym) {
+      // eigvalss gate + mirror (src/eigensolver.cpp:98-111) ahead of the
+      // steady-state test; mirroring keeps a moderate record moderate.
+      sym_ok = !not_symmetric(m);
+      m[3] = m[1];
+      m[6] = m[2];
+      m[7] = m[5];
+    }
+    if (sym_ok && mod && pfast) {
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
@@ -281,10 +290,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+      if (MODE == kSym) f = 0;
       bad = false;
     } else {
       L = stage2(pc, pmod, pbad, T);
-      stage1<MODE, WANT_FLAGS>(m, mod, v, nc, f, bad);
+      if (MODE == kSym) {
+        // already mirrored: the gate verdict decides, stage 1 must not re-test
+        bad = !sym_ok;
+        f = bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
+        if (bad) {
+          const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+          v.i1 = v.j2 = v.j3 = v.disc = qnan;
+          mod = false;
+        } else {
+          v = mod ? invariants_moderate(m) : invariants(m);
+        }
+        nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+      } else {
+        stage1<MODE, WANT_FLAGS>(m, mod, v, nc, f, bad);
+      }
     }
     store_lam(L);
     store_stage1(r, valid);

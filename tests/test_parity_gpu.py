@@ -261,3 +261,88 @@ def test_study_variants_on_device():
     R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(w) for w in want), U.nthreads())
     for got, w in zip((j2, j3, jd), want):
         assert U.bit_equal(got.reshape(n, 9), w).all()
+
+
+# ---- properties the reference's own tests assert, re-run on GPU outputs ----
+
+def _mm(x, y):
+    """Reference matmul association (src/mat3.cpp:18-26), batched."""
+    return ((x[:, :, 0, None] * y[:, None, 0, :] + x[:, :, 1, None] * y[:, None, 1, :])
+            + x[:, :, 2, None] * y[:, None, 2, :])
+
+
+def _inv_adj(v):
+    """Reference inverse_adjugate (src/mat3.cpp:49-64), batched."""
+    c = np.empty_like(v)
+    c[:, 0, 0] = v[:, 1, 1] * v[:, 2, 2] - v[:, 1, 2] * v[:, 2, 1]
+    c[:, 0, 1] = v[:, 1, 2] * v[:, 2, 0] - v[:, 1, 0] * v[:, 2, 2]
+    c[:, 0, 2] = v[:, 1, 0] * v[:, 2, 1] - v[:, 1, 1] * v[:, 2, 0]
+    c[:, 1, 0] = v[:, 0, 2] * v[:, 2, 1] - v[:, 0, 1] * v[:, 2, 2]
+    c[:, 1, 1] = v[:, 0, 0] * v[:, 2, 2] - v[:, 0, 2] * v[:, 2, 0]
+    c[:, 1, 2] = v[:, 0, 1] * v[:, 2, 0] - v[:, 0, 0] * v[:, 2, 1]
+    c[:, 2, 0] = v[:, 0, 1] * v[:, 1, 2] - v[:, 0, 2] * v[:, 1, 1]
+    c[:, 2, 1] = v[:, 0, 2] * v[:, 1, 0] - v[:, 0, 0] * v[:, 1, 2]
+    c[:, 2, 2] = v[:, 0, 0] * v[:, 1, 1] - v[:, 0, 1] * v[:, 1, 0]
+    det = (v[:, 0, 0] * (v[:, 1, 1] * v[:, 2, 2] - v[:, 1, 2] * v[:, 2, 1])
+           - v[:, 0, 1] * (v[:, 1, 0] * v[:, 2, 2] - v[:, 1, 2] * v[:, 2, 0])) \
+        + v[:, 0, 2] * (v[:, 1, 0] * v[:, 2, 1] - v[:, 1, 1] * v[:, 2, 0])
+    return np.transpose(c, (0, 2, 1)) / det[:, None, None], det
+
+
+def test_acceptance_c9_ordering_and_trace_on_1e6_spectra():
+    """proj/tests/acceptance/acceptance.cpp:244-265 (C9): ascending order and
+    trace consistency on 10^6 random similarity transforms."""
+    rng = np.random.default_rng(9)
+    n = 1_000_000
+    m = rng.uniform(-1, 1, (int(n * 1.2), 3, 3))
+    minv, det = _inv_adj(m)
+    keep = np.abs(det) >= 1e-2
+    m, minv = m[keep][:n], minv[keep][:n]
+    d = rng.uniform(-5, 5, (n, 3))
+    a = _mm(m * d[:, None, :], minv).reshape(n, 9)
+    lam, inv, _ = _run(a, flags=False)
+    assert ((lam[:, 0] <= lam[:, 1]) & (lam[:, 1] <= lam[:, 2])).all()
+    i1 = inv[:, 0]
+    spread = 2.0 * np.sqrt(3.0 * np.maximum(inv[:, 1], 0.0))
+    s = (lam[:, 0] + lam[:, 1]) + lam[:, 2]
+    assert (np.abs(s - i1) <= 20 * 2.0 ** -53 * (np.abs(i1) + spread)).all()
+
+
+def test_scaled_identities_exact():
+    """test_eigensolver.cpp:41-52 and acceptance C2: lambda == alpha bitwise,
+    j2 = j3 = disc = 0, no advisory, for alpha = mant*2^[-30,30] and 10^U[-100,100]."""
+    rng = np.random.default_rng(2)
+    al = np.concatenate([np.ldexp(rng.uniform(-1, 1, 5000), rng.integers(-30, 31, 5000)),
+                         10.0 ** rng.uniform(-100, 100, 5000)])
+    a = np.zeros((al.size, 9))
+    a[:, 0] = a[:, 4] = a[:, 8] = al
+    lam, inv, flags = _run(a)
+    assert (lam == al[:, None]).all() and (inv[:, 1:] == 0).all() and not (flags & 1).any()
+
+
+def test_shift_equivariance():
+    """test_eigensolver.cpp:104-128: entries and shifts on a 2^-20 grid, worst
+    |(l(A)+beta) - l(A+beta I)| / (eps*(|beta| + ||A||_F)) <= 30."""
+    rng = np.random.default_rng(33)
+    n = 200_000
+    snap = lambda x: np.ldexp(np.round(np.ldexp(x, 20)), -20)
+    a = snap(rng.uniform(-4, 4, (n, 9)))
+    beta = snap(rng.uniform(-4, 4, n))
+    sh = a.copy()
+    sh[:, [0, 4, 8]] += beta[:, None]
+    l0, _, _ = _run(a, inv=False, flags=False)
+    l1, _, _ = _run(sh, inv=False, flags=False)
+    scale = 2.0 ** -53 * (np.abs(beta) + np.sqrt((a * a).sum(1)))
+    diff = np.abs((l0 + beta[:, None]) - l1).max(1)
+    assert (diff / scale).max() <= 30.0
+
+
+def test_eigvalss_tight_symmetric_cluster():
+    """test_eigensolver.cpp:140-146: spectrum error <= 10 eps ||A||_F on
+    U diag(1,1,1+1e-12) U^T (Symm transform, bench.cpp:53-60)."""
+    q = np.sqrt(2.0) / 2.0
+    u = np.array([[q, -0.5, 0.5], [q, 0.5, -0.5], [0.0, q, q]])
+    d = np.diag([1.0, 1.0, 1.0 + 1e-12])
+    a = _mm(_mm(u[None], d[None]), u.T[None]).reshape(1, 9)
+    lam = eig.eigvalss(a).lam[0]
+    assert np.abs(lam - [1.0, 1.0, 1.0 + 1e-12]).max() <= 10 * 2.0 ** -53 * np.sqrt((a * a).sum())

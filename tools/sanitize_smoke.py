@@ -1,0 +1,34 @@
+"""Small workload touching every kernel and code path (TMA ring, ragged tails,
+misaligned coalesced path, advisory, eigvalss, study kernels, generator) for
+compute-sanitizer runs.  Exits 0 on success."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2511_00292_b200 as eig
+from tests import _util as U
+
+for n in (1, 33, 64, 65, 1000, 4099):
+    a = torch.from_numpy(U.mixed_corpus(max(n, 8), n)[:n]).cuda()
+    eig.eigvals(a, return_invariants=True, return_flags=True)
+    eig.eigvalss(a, return_invariants=True, return_flags=True)
+    eig.invariants(a)
+    buf = torch.empty(n * 9 + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = a.reshape(-1)
+    eig.eigvals(buf[1:].view(n, 9), return_flags=True)
+for cfg in range(1, 6):
+    g = eig.generate(cfg, 3000, seed=cfg)
+    eig.eigvals(g, return_flags=True)
+j3 = torch.randn(1000, dtype=torch.float64, device="cuda")
+eig.triple_angle(j3, torch.randn(1000, dtype=torch.float64, device="cuda"))
+a = U.mixed_corpus(2000, 3)
+eig.invariants(a, variant="Naive")
+eig.invariants(a, variant="NaiveTensor")
+eig.eigvals_naive(a, return_flags=True)
+eig.jacobians(a)
+eig.eigvals(a)  # host pipeline
+torch.cuda.synchronize()
+print("sanitize smoke ok")

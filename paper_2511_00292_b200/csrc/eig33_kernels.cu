@@ -87,13 +87,35 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         : "memory");
   } while (!done);
 }
+#ifndef EIG33_STREAM_HINTS
+#define EIG33_STREAM_HINTS 0
+#endif
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           unsigned long long* b) {
+#if EIG33_STREAM_HINTS
+  // input records are read exactly once: evict them from L2 first
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(b))
       : "memory");
+#endif
+}
+// lambda / invariant stores: written once, never re-read by this kernel
+__device__ __forceinline__ void st_out(double* p, double v) {
+#if EIG33_STREAM_HINTS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
 }
 
 __device__ __forceinline__ void load_tables(double* tab) {
@@ -260,9 +282,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   };
   auto store_lam = [&](const Lam& L) {
     if (!pvalid) return;
-    lam[pr * 3 + 0] = L.l1;
-    lam[pr * 3 + 1] = L.l2;
-    lam[pr * 3 + 2] = L.l3;
+    st_out(lam + pr * 3 + 0, L.l1);
+    st_out(lam + pr * 3 + 1, L.l2);
+    st_out(lam + pr * 3 + 2, L.l3);
   };
   // One step of the record pipeline: stage 2 of the carried record, stage 1 of m.
   auto step = [&](long long r, bool valid) {

@@ -222,7 +222,6 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
   mod = is_moderate(m);
-  if (!mod) mod = is_moderate_or_zero(m);
 }
 template <bool TMA>
 __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
@@ -300,12 +299,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       m[6] = m[2];
       m[7] = m[5];
     }
-    // Warp-uniform tier choice (no divergence inside a tier):
-    //   A  every lane moderate, carried record j2 > 0 and disc > 0: eig_fast
-    //   B  every lane moderate (zeros allowed): branch-free eig_moderate_bl
-    //   C  otherwise: per-lane checked reference-order path
-    const bool lane_mod = sym_ok && mod && pmod;
-    if (__all_sync(0xffffffffu, lane_mod && pfast)) {
+    if (sym_ok && mod && pfast) {
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
@@ -317,15 +311,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       L = eig_fast(pc, T.tab);
 #endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
-      if (MODE == kSym) f = 0;
       nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
-      bad = false;
-    } else if (__all_sync(0xffffffffu, lane_mod)) {
-      L = eig_moderate_bl(pc, T.tab);
-      v = invariants_moderate(m);
-      if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       if (MODE == kSym) f = 0;
-      nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
       bad = false;
     } else {
       L = stage2(pc, pmod, pbad, T);

@@ -40,8 +40,8 @@ constexpr int kWarps = kThreads / 32;
 #ifndef EIG33_RPL
 #define EIG33_RPL 2
 #endif
-constexpr int kRPL = EIG33_RPL;  // records per lane per chunk (1 or 2)
-static_assert(kRPL == 1 || kRPL == 2, "kRPL must be 1 or 2");
+constexpr int kRPL = EIG33_RPL;  // records per lane per chunk (1, 2 or 4)
+static_assert(kRPL == 1 || kRPL == 2 || kRPL == 4, "kRPL must be 1, 2 or 4");
 constexpr int kChunk = 32 * kRPL;  // records per warp chunk
 #ifndef EIG33_STAGES
 #define EIG33_STAGES (4 / EIG33_RPL)
@@ -353,23 +353,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   pr = gw * kChunk + lane;
   pvalid = lane < cnt;
   store_stage1(pr, pvalid);
-  if (kRPL == 2) {
-    ring_read(buf, lane, 1, m, mod);
-    ring_release<TMA>(R, gw, 0, buf);
-    step(gw * kChunk + 32 + lane, 32 + lane < cnt);
+#pragma unroll
+  for (int h = 1; h < kRPL; ++h) {
+    ring_read(buf, lane, h, m, mod);
+    if (h == kRPL - 1) ring_release<TMA>(R, gw, 0, buf);
+    step(gw * kChunk + 32 * h + lane, 32 * h + lane < cnt);
   }
 
   uint32_t it = 1;
   for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
     buf = ring_acquire<TMA>(R, c, it, cnt);
     const long long base = c * kChunk + lane;
-    ring_read(buf, lane, 0, m, mod);
-    if (kRPL == 1) ring_release<TMA>(R, c, it, buf);
-    step(base, lane < cnt);
-    if (kRPL == 2) {
-      ring_read(buf, lane, 1, m, mod);
-      ring_release<TMA>(R, c, it, buf);
-      step(base + 32, 32 + lane < cnt);
+#pragma unroll
+    for (int h = 0; h < kRPL; ++h) {
+      ring_read(buf, lane, h, m, mod);
+      if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
+      step(base + 32 * h, 32 * h + lane < cnt);
     }
   }
   store_lam(stage2(pc, pmod, pbad, T));

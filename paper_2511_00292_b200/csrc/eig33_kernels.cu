@@ -222,6 +222,9 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
   mod = is_moderate(m);
+#if EIG33_MODERATE_ZEROS
+  if (!mod) mod = is_moderate_or_zero(m);
+#endif
 }
 template <bool TMA>
 __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,

@@ -13,23 +13,25 @@ using namespace eig33b;
 extern "C" {
 // path: 0 = dispatch like the kernel (moderate fast path when is_moderate),
 //       1 = always the checked general path, 2 = always the moderate path
+static bool moderate(const double* m) { return is_moderate(m) || is_moderate_or_zero(m); }
 static Inv inv_path(const double* m, int path) {
-  if (path == 2 || (path == 0 && is_moderate(m))) return invariants_moderate(m);
+  if (path == 2 || (path == 0 && moderate(m))) return invariants_moderate(m);
   return invariants(m);
 }
 static Lam lam_path(const double* m, const Inv& v, int path) {
-  if (path == 2 || (path == 0 && is_moderate(m)))
+  if (path == 2 || (path == 0 && moderate(m)))
     return from_invariants_moderate(m, v, eig33_tab);
   return from_invariants(m, v, eig33_tab);
 }
 int hm_is_moderate(const double* a) { return is_moderate(a) ? 1 : 0; }
+int hm_is_moderate_or_zero(const double* a) { return is_moderate_or_zero(a) ? 1 : 0; }
 // path 3: the kernel's steady-state block (eig_fast) where its preconditions
 // hold (moderate, j2 > 0, disc > 0), else path 0
 void hm_eigvals_fast(const double* a, size_t n, double* lam) {
   for (size_t i = 0; i < n; ++i) {
     const double* m = a + 9 * i;
     Lam l;
-    if (is_moderate(m)) {
+    if (moderate(m)) {
       const Inv v = invariants_moderate(m);
       const Carry c{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
       l = fast_carry(v) ? eig_fast(c, eig33_tab) : eig_moderate_bl(c, eig33_tab);

@@ -122,3 +122,28 @@ def test_product_study_variants_bitwise():
     R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[3:]), U.nthreads())
     for k in range(3):
         assert U.bit_equal(js[k], js[k + 3]).all()
+
+
+def test_moderate_tier_with_exact_zeros_is_bitwise():
+    """The moderate CSE/guard-free tier admits exact zeros (a zero is a multiple
+    of every grain): sparse, diagonal, exact-repeated and near-identity records
+    forced through it reproduce the reference bits."""
+    rng = np.random.default_rng(41)
+    n = 1 << 18
+    a = rng.standard_normal((n, 9))
+    a[rng.random((n, 9)) < 0.35] = 0.0                      # sparse
+    a[: n // 8, [1, 2, 3, 5, 6, 7]] = 0.0                    # diagonal
+    a[n // 8: n // 4] = np.round(a[n // 8: n // 4] * 64) / 64  # grid, ties, cancellations
+    b = a[n // 4: n // 2]                                    # symmetric, some zeros
+    b[:, [3, 6, 7]] = b[:, [1, 2, 5]]
+    a = np.ascontiguousarray(a)
+    H = U.hostmath()
+    ok = np.array([H.hm_is_moderate_or_zero(U.ptr(a[i])) for i in range(0, n, 997)])
+    assert ok.mean() > 0.95
+    inv = np.empty((n, 4))
+    H.hm_invariants(U.ptr(a), U.S(n), U.ptr(inv))  # dispatches like the kernel
+    assert U.bit_equal(inv, U.checker_invariants(a)).all()
+    lam = np.empty((n, 3))
+    H.hm_eigvals_fast(U.ptr(a), U.S(n), U.ptr(lam))
+    lam_r, _ = U.checker_eigvals(a, adv=False)
+    assert (U.lam_error_units(lam, lam_r) <= U.TOL_UNITS).all()

@@ -165,6 +165,58 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
   return from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
 }
 
+// Out-of-line tiers of the record pipeline.  Kept as real calls so that their
+// register demand never enters the allocation of the steady-state loop (an
+// inlined second tier made ptxas move arrays to local memory there and cost 3x).
+struct M9 {
+  double e[9];
+};
+struct StepOut {
+  Lam L;
+  Inv v;
+  uint8_t f;
+  bool bad, mod;
+};
+
+// Tier B, warp-uniform: every lane moderate but some carried record has
+// j2 <= 0 or disc <= 0: branch-free eig_moderate_bl interleaved with the DAG.
+template <int MODE, bool WANT_FLAGS>
+__device__ __noinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
+  StepOut o;
+  o.L = eig_moderate_bl(pc, tab);
+  o.v = invariants_moderate(mm.e);
+  o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
+  o.bad = false;
+  o.mod = true;
+  return o;
+}
+
+// Tier C, per lane: the checked reference-order path (zeros, subnormals,
+// extreme exponents, inf/NaN, eigvalss rejects).
+template <int MODE, bool WANT_FLAGS>
+__device__ __noinline__ StepOut tier_general(M9 mm, bool sym_ok, bool mod, Carry pc, bool pmod,
+                                             bool pbad, const double* tab) {
+  StepOut o;
+  o.L = stage2(pc, pmod, pbad, Tabs{tab});
+  if (MODE == kSym) {
+    o.bad = !sym_ok;  // already mirrored: the gate verdict decides
+    o.f = o.bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
+    o.mod = mod && !o.bad;
+    if (o.bad) {
+      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+      o.v.i1 = o.v.j2 = o.v.j3 = o.v.disc = qnan;
+    } else {
+      o.v = mod ? invariants_moderate(mm.e) : invariants(mm.e);
+    }
+  } else {
+    Carry nc;
+    bool m2 = mod;
+    stage1<MODE, WANT_FLAGS>(mm.e, m2, o.v, nc, o.f, o.bad);
+    o.mod = m2;
+  }
+  return o;
+}
+
 // Per-warp record pipeline.  Work unit = a chunk of 32 consecutive records,
 // one per lane.  Lane 0 streams the warp's chunks HBM -> SMEM with
 // cp.async.bulk into a kStages-deep per-warp ring completed on per-warp
@@ -302,7 +354,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       m[6] = m[2];
       m[7] = m[5];
     }
-    if (sym_ok && mod && pfast) {
+    // Warp-uniform tier choice, so a warp never runs two tiers for one step.
+    if (__all_sync(0xffffffffu, sym_ok && mod && pfast)) {
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
@@ -314,27 +367,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       L = eig_fast(pc, T.tab);
 #endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
-      nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
       if (MODE == kSym) f = 0;
       bad = false;
     } else {
-      L = stage2(pc, pmod, pbad, T);
-      if (MODE == kSym) {
-        // already mirrored: the gate verdict decides, stage 1 must not re-test
-        bad = !sym_ok;
-        f = bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
-        if (bad) {
-          const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-          v.i1 = v.j2 = v.j3 = v.disc = qnan;
-          mod = false;
-        } else {
-          v = mod ? invariants_moderate(m) : invariants(m);
-        }
-        nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
-      } else {
-        stage1<MODE, WANT_FLAGS>(m, mod, v, nc, f, bad);
-      }
+      M9 mm;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) mm.e[k] = m[k];
+      StepOut o;
+      if (__all_sync(0xffffffffu, sym_ok && mod && pmod))
+        o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
+      else
+        o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pmod, pbad, T.tab);
+      L = o.L;
+      v = o.v;
+      f = o.f;
+      bad = o.bad;
+      mod = o.mod;
     }
+    nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
     store_lam(L);
     store_stage1(r, valid);
     pc = nc;

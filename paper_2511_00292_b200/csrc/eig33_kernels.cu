@@ -168,6 +168,9 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
 // Out-of-line tiers of the record pipeline.  Kept as real calls so that their
 // register demand never enters the allocation of the steady-state loop (an
 // inlined second tier made ptxas move arrays to local memory there and cost 3x).
+#ifndef EIG33_TIER_B_INLINE
+#define EIG33_TIER_B_INLINE __noinline__
+#endif
 struct M9 {
   double e[9];
 };
@@ -181,7 +184,7 @@ struct StepOut {
 // Tier B, warp-uniform: every lane moderate but some carried record has
 // j2 <= 0 or disc <= 0: branch-free eig_moderate_bl interleaved with the DAG.
 template <int MODE, bool WANT_FLAGS>
-__device__ __noinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
+__device__ EIG33_TIER_B_INLINE StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
   StepOut o;
   o.L = eig_moderate_bl(pc, tab);
   o.v = invariants_moderate(mm.e);

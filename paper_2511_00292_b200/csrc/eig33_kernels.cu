@@ -239,6 +239,7 @@ __device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
       const long long c = gw + (long long)s * R.W;
       if (c < R.full) {
         mbar_expect_tx(&R.bars[s], kChunkBytes);
+        EIG33_CHECK((c + 1) * kChunk <= R.n);
         bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
       }
     }
@@ -290,6 +291,7 @@ __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uin
     const long long nc = c + (long long)kStages * R.W;
     if (nc < R.full) {
       mbar_expect_tx(&R.bars[stage], kChunkBytes);
+      EIG33_CHECK((nc + 1) * kChunk <= R.n);
       bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
     }
   }
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   long long pr;  // record index of the carried stage
   auto store_stage1 = [&](long long r, bool valid) {
     if (!valid) return;
+    EIG33_CHECK(r >= 0 && r < R.n);
     if (WANT_INV) {
       inv[r * 4 + 0] = v.i1;
       inv[r * 4 + 1] = v.j2;
@@ -340,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   };
   auto store_lam = [&](const Lam& L) {
     if (!pvalid) return;
+    EIG33_CHECK(pr >= 0 && pr < R.n);
     st_out(lam + pr * 3 + 0, L.l1);
     st_out(lam + pr * 3 + 1, L.l2);
     st_out(lam + pr * 3 + 2, L.l3);

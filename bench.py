@@ -357,10 +357,27 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
         same = bool(torch.equal(h_l.view(torch.int64), lam[:ne].cpu().view(torch.int64)))
-        e2e = {"value": ne * world * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": ne * 72,
+        # PCIe roof for this path: plain pinned H2D copy bandwidth on this box
+        probe = h_a.view(-1)[: min(h_a.numel(), 1 << 28)]
+        dst = torch.empty(probe.numel(), dtype=probe.dtype, device=dev)
+        dst.copy_(probe, non_blocking=True)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(3):
+            dst.copy_(probe, non_blocking=True)
+        c1.record()
+        c1.synchronize()
+        h2d_gbs = 3 * probe.numel() * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del dst, probe
+        e2e_value = ne * world * args.e2e_steps / el
+        e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * 72,
                "d2h_bytes_per_step": ne * 24, "steps": args.e2e_steps, "records_per_gpu_per_step": ne,
                "api": "eig33_eigvals_host (pinned host buffers, chunked H2D/kernel/D2H over 3 streams)",
-               "bitwise_equal_to_device_path": same}
+               "bitwise_equal_to_device_path": same,
+               "pcie_roofline": {"bound": "pcie_h2d", "h2d_gbs_measured": h2d_gbs,
+                                 "achieved_h2d_gbs": e2e_value / world * 72 / 1e9,
+                                 "frac": e2e_value / world * 72 / 1e9 / h2d_gbs}}
         del h_a, h_l
 
     if rank != 0:

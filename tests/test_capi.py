@@ -55,3 +55,14 @@ def test_shape_validation_mirrors_reference_to_mat(shape):
         return
     with pytest.raises(ValueError):
         eig._records_np(np.zeros(shape))
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
+def test_cxx_header_compiles_against_reference_types():
+    """Drop-in: with the reference's own headers on the include path, batch.hpp
+    adds its overloads to the reference's Mat3 / InvariantSet / EigenTriple."""
+    import subprocess
+    src = os.path.join(U.ROOT, "tests", "cpp", "batch_api_check.cpp")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(U.ROOT, "include"),
+                        "-I", "/root/reference/proj/include", src], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

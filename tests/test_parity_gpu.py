@@ -369,3 +369,17 @@ def test_eigvalss_tight_symmetric_cluster():
     a = _mm(_mm(u[None], d[None]), u.T[None]).reshape(1, 9)
     lam = eig.eigvalss(a).lam[0]
     assert np.abs(lam - [1.0, 1.0, 1.0 + 1e-12]).max() <= 10 * 2.0 ** -53 * np.sqrt((a * a).sum())
+
+
+def test_signed_zeros_and_sparse_records():
+    """Exact +-0 entries go through the moderate tiers (a zero is a multiple of
+    every grain); signs of zero must survive into j3/disc and the triple angle
+    (atan2(+0, -0) = pi) exactly as in the reference."""
+    rng = np.random.default_rng(71)
+    n = 1 << 18
+    a = np.round(rng.standard_normal((n, 9)) * 8) / 8
+    z = rng.random((n, 9)) < 0.4
+    a[z] = np.where(rng.random(z.sum()) < 0.5, 0.0, -0.0)
+    a[: n // 16] = np.where(rng.random((n // 16, 9)) < 0.5, 0.0, -0.0)  # all-zero records
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, "signed-zeros")

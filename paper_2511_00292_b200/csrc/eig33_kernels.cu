@@ -22,6 +22,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #define EIG33_TABLE_DECL static __constant__
@@ -534,11 +536,16 @@ static int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
   return code;
 }
 
+// Per-device launch geometry, computed once per kernel instantiation.  Host
+// threads may launch concurrently (the multi-GPU driver runs one per device),
+// so the first-use initialisation is serialised; the values are read back
+// through atomics afterwards.
 struct DevInfo {
-  int sms = 0;
-  int occ[3][2][2][2] = {};
+  std::atomic<int> sms{0};
+  std::atomic<int> occ[3][2][2][2] = {};
 };
 static DevInfo g_dev[64];
+static std::mutex g_dev_mu;
 
 template <int MODE, bool TMA, bool WI, bool WF>
 static int launch_fused(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
@@ -550,22 +557,30 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   DevInfo& d = g_dev[dev];
   const size_t smem = sizeof(Smem);
   auto kern = MODE == kInv ? k_invariants<TMA> : k_fused<MODE, TMA, WI, WF>;
-  int& occ = d.occ[MODE][TMA][WI][WF];
+  std::atomic<int>& occ_slot = d.occ[MODE][TMA][WI][WF];
+  int occ = occ_slot.load(std::memory_order_acquire);
   if (!occ) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaFuncSetAttribute", e);
-    int o = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
-    if (e != cudaSuccess) return fail(EIG33_ECUDA, "occupancy query", e);
-    if (!d.sms) {
-      e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
-      if (e != cudaSuccess) return fail(EIG33_ECUDA, "SM count", e);
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    occ = occ_slot.load(std::memory_order_relaxed);
+    if (!occ) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaFuncSetAttribute", e);
+      int o = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
+      if (e != cudaSuccess) return fail(EIG33_ECUDA, "occupancy query", e);
+      if (!d.sms.load()) {
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return fail(EIG33_ECUDA, "SM count", e);
+        d.sms.store(sms);
+      }
+      occ = o > 0 ? o : 1;
+      occ_slot.store(occ, std::memory_order_release);
     }
-    occ = o > 0 ? o : 1;
   }
   const long long nchunks = (long long)((n + kChunk - 1) / kChunk);
   const long long nblk = (nchunks + kWarps - 1) / kWarps;  // at least one chunk per warp
-  const long long cap = (long long)d.sms * occ;
+  const long long cap = (long long)d.sms.load() * occ;
   const long long grid = nblk < cap ? nblk : cap;
   kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);
   e = cudaGetLastError();
@@ -595,7 +610,7 @@ static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t
 static int launch_advisory(const double* a, size_t n, uint8_t* flags, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
-  int sms = g_dev[dev].sms;
+  int sms = (dev >= 0 && dev < 64) ? g_dev[dev].sms.load() : 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long windows = (long long)((n + kAdvWindow - 1) / kAdvWindow);
   const long long grid = windows < 4LL * sms ? windows : 4LL * sms;

@@ -383,3 +383,33 @@ def test_signed_zeros_and_sparse_records():
     a[: n // 16] = np.where(rng.random((n // 16, 9)) < 0.5, 0.0, -0.0)  # all-zero records
     lam, inv, flags = _run(a)
     _assert_parity(a, lam, inv, flags, "signed-zeros")
+
+
+def test_concurrent_host_threads_and_streams():
+    """The C ABI is reentrant: host threads calling the host-buffer API and
+    device calls on independent streams give the single-call bits."""
+    import threading
+
+    a = U.mixed_corpus(1 << 18, 81)
+    want = eig.eigvals(a, return_invariants=True)
+    res = [None] * 4
+
+    def work(i):
+        res[i] = eig.eigvals(a, return_invariants=True)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in res:
+        assert U.bit_equal(r.lam, want.lam).all() and U.bit_equal(r.inv, want.inv).all()
+    d = _dev(a)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = []
+    for s in streams:
+        with torch.cuda.stream(s):
+            outs.append(eig.eigvals(d).lam)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert U.bit_equal(o.cpu().numpy(), want.lam).all()

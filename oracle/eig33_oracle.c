@@ -426,3 +426,46 @@ void orc_jacobians(const double *a, size_t n, double *jj2, double *jj3, double *
     }
   }
 }
+
+/* ---- paper corpora: make_transform / generate_case (src/bench.cpp:53-75) ---- */
+
+/* src/mat3.cpp:18-26 */
+static void orc_matmul(const double *a, const double *b, double *c) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      c[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+
+/* src/mat3.cpp:49-64 (transpose of the cofactor matrix over det) */
+static void orc_inverse_adjugate(const double *a, double *inv) {
+  const double det = a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+                     a[2] * (a[3] * a[7] - a[4] * a[6]);
+  double c[9];
+  orc_cofactor(a, c);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) inv[3 * i + j] = c[3 * j + i] / det;
+}
+
+/* path 0 = D1, 1 = D2; kind 0 = Symm, 1 = U1, 2 = U2(gamma); one record per delta */
+void orc_generate_case(int path, int kind, double gamma, const double *deltas, size_t n,
+                       double *out) {
+  const double q = 0x1.6a09e667f3bcdp-1; /* std::numbers::sqrt2_v<double> / 2.0 */
+  double u[9];
+  if (kind == 0) {
+    const double s[9] = {q, -0.5, 0.5, q, 0.5, -0.5, 0.0, q, q};
+    memcpy(u, s, sizeof u);
+  } else if (kind == 1) {
+    const double s[9] = {1, -1, 1, 1, 1, 1, -1, -1, 1};
+    memcpy(u, s, sizeof u);
+  } else {
+    const double s[9] = {1, 1, 1, 1, 0, 1, 2, 1, 2.0 + gamma};
+    memcpy(u, s, sizeof u);
+  }
+  double uinv[9], ud[9];
+  orc_inverse_adjugate(u, uinv);
+  for (size_t i = 0; i < n; ++i) {
+    const double d[9] = {path == 0 ? 1.0 : -1.0, 0, 0, 0, 1.0, 0, 0, 0, 1.0 + deltas[i]};
+    orc_matmul(u, d, ud);
+    orc_matmul(ud, uinv, out + 9 * i);
+  }
+}

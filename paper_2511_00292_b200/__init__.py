@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = [
     "eigvals", "eigvalss", "invariants", "triple_angle", "generate", "multi_eigvals",
-    "eigvals_naive", "jacobians", "VARIANTS",
+    "eigvals_naive", "jacobians", "VARIANTS", "generate_case", "default_delta_grid",
     "lib", "EigResult", "eps_mach", "FLAG_ADVISORY", "FLAG_NOT_SYMMETRIC",
 ]
 
@@ -45,6 +45,7 @@ C_ABI_SYMBOLS = (
     "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
     "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
     "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
+    "eig33cu_generate_case",
 )
 VARIANTS = {"Stable": 0, "Naive": 1, "NaiveTensor": 2}  # reference AlgorithmVariant
 
@@ -77,6 +78,7 @@ def lib() -> ctypes.CDLL:
         "eig33cu_invariants_variant": ([P, S, I, P, P], I),
         "eig33cu_eigvals_naive": ([P, S, P, P, P], I),
         "eig33cu_jacobians": ([P, S, P, P, P, P], I),
+        "eig33cu_generate_case": ([I, I, ctypes.c_double, P, S, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -304,6 +306,29 @@ def generate(config: int, n: int, seed: int = 0, first_index: int = 0, device="c
     with torch.cuda.device(out.device):
         _check(lib().eig33cu_generate(int(config), int(seed) & (2**64 - 1), int(first_index), int(n),
                                       _ptr(out), _stream(out)), "generate")
+    return out
+
+
+PATHS = {"D1": 0, "D2": 1}                    # reference PathKind (bench.hpp:21)
+TRANSFORMS = {"Symm": 0, "U1": 1, "U2": 2}    # reference Transform::Kind (bench.hpp:28-31)
+
+
+def default_delta_grid():
+    """The reference's sweep grid 10^(-k/4), k = 4..64 (src/bench.cpp:77-82)."""
+    return [10.0 ** (-k / 4.0) for k in range(4, 65)]
+
+
+def generate_case(path: str, transform: str, deltas, gamma: float = 1e-3, device="cuda"):
+    """Batched ``eig33::bench::generate_case`` (reference src/bench.cpp:53-75):
+    one (n,9) CUDA record per delta, bit-identical to the reference."""
+    torch = _torch()
+    if path not in PATHS or transform not in TRANSFORMS:
+        raise ValueError("path must be D1/D2 and transform Symm/U1/U2")
+    d = torch.as_tensor(np.asarray(deltas, dtype=np.float64).reshape(-1), device=device)
+    out = torch.empty((d.numel(), 9), dtype=torch.float64, device=device)
+    with torch.cuda.device(out.device):
+        _check(lib().eig33cu_generate_case(PATHS[path], TRANSFORMS[transform], float(gamma), _ptr(d),
+                                           d.numel(), _ptr(out), _stream(out)), "generate_case")
     return out
 
 

@@ -17,6 +17,10 @@ P = ctypes.c_void_p
 S = ctypes.c_size_t
 
 
+def ctypes_double(x):
+    return ctypes.c_double(x)
+
+
 def ptr(x):
     return None if x is None else x.ctypes.data_as(ctypes.c_void_p)
 

@@ -159,3 +159,12 @@ def test_port_study_variants_bitwise_equal_compiled_reference():
     R.ref_jacobians(U.ptr(a), U.S(n), *(U.ptr(j) for j in js[3:]), U.nthreads())
     for k in range(3):
         assert U.bit_equal(js[k], js[k + 3]).all()
+
+
+def test_port_generate_case_reproduces_perf_matrix():
+    """generate_case(D2, U1, 1e-14) is the paper's perf matrix (bench.cpp:69-75,
+    test_bench.cpp:62-74); its invariants carry the Appendix B bits."""
+    out = np.empty((1, 9))
+    d = np.array([1e-14])
+    U.port().orc_generate_case(1, 1, U.ctypes_double(1e-3), U.ptr(d), U.S(1), U.ptr(out))
+    assert U.bit_equal(out[0], U.perf_matrix()).all()

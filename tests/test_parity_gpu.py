@@ -413,3 +413,18 @@ def test_concurrent_host_threads_and_streams():
     torch.cuda.synchronize()
     for o in outs:
         assert U.bit_equal(o.cpu().numpy(), want.lam).all()
+
+
+def test_generate_case_matches_port_bitwise():
+    """Batched paper corpora (src/bench.cpp:53-82) on the device equal the C
+    restatement bit for bit for every path x transform over the reference grid."""
+    deltas = np.array(eig.default_delta_grid() + [0.0, 1e-14, 0.5, 3.0])
+    for path, pi in eig.PATHS.items():
+        for kind, ki in eig.TRANSFORMS.items():
+            got = eig.generate_case(path, kind, deltas, gamma=1e-3).cpu().numpy()
+            want = np.empty((deltas.size, 9))
+            U.port().orc_generate_case(pi, ki, U.ctypes_double(1e-3), U.ptr(deltas), U.S(deltas.size),
+                                       U.ptr(want))
+            assert U.bit_equal(got, want).all(), (path, kind)
+    with pytest.raises(ValueError):
+        eig.generate_case("D1", "U2", deltas, gamma=0.0)

@@ -428,3 +428,23 @@ def test_generate_case_matches_port_bitwise():
             assert U.bit_equal(got, want).all(), (path, kind)
     with pytest.raises(ValueError):
         eig.generate_case("D1", "U2", deltas, gamma=0.0)
+
+
+def test_reference_eigensolver_known_answers():
+    """proj/tests/test_eigensolver.cpp:54-69, 130-137 on the device:
+    U1 similarity within 100 kappa2 ||A||_F eps; the D2/U1/1e-14 perf matrix
+    within 1e-14 of the exact spectrum; eigvalss(diag(1,2,3)) within 12 eps."""
+    from tests import _exact
+
+    u1 = np.array([[1, -1, 1], [1, 1, 1], [-1, -1, 1]], dtype=np.float64)
+    a = eig.generate_case("D1", "U1", [1.0]).cpu().numpy()  # U1 diag(1,1,2) U1^-1
+    a2 = _mm(_mm(u1[None], np.diag([-1.0, 1.0, 2.0])[None]), _inv_adj(u1[None])[0]).reshape(1, 9)
+    lam = eig.eigvals(a2).lam[0]
+    kappa2 = np.linalg.cond(u1, 2)
+    assert np.abs(lam - [-1, 1, 2]).max() <= 100 * kappa2 * np.sqrt((a2 * a2).sum()) * 2.0 ** -53
+    pm = eig.generate_case("D2", "U1", [1e-14]).cpu().numpy()
+    ex = [float(x) for x in _exact.exact_spectrum(pm[0])]
+    assert np.abs(eig.eigvals(pm).lam[0] - ex).max() <= 1e-14
+    lam_s = eig.eigvalss(np.diag([1.0, 2.0, 3.0])).lam[0]
+    assert np.abs(lam_s - [1, 2, 3]).max() <= 12 * 2.0 ** -53
+    assert a.shape == (1, 9)

@@ -1,23 +1,23 @@
 // eig33_kernels.cu -- sm_100a kernels and device-pointer C ABI of the batched
-// eig33 hot path (see include/eig33_cuda.h and DESIGN.md).
+// eig33 hot path (see include/eig33_cuda.h and DESIGN.md section 3).
 //
 // MUST be compiled with --fmad=false: the invariant arithmetic is bit-exact
 // against the reference only without contraction (proj/src/CMakeLists.txt:9-10).
 //
 // Kernel map
-//   k_fused<MODE, TMA>   one persistent kernel for eigvals / invariants /
-//                        eigvalss: 256 records per tile, one record per thread.
-//                        Input tiles (256 x 72 B = 18 KB) stream HBM -> SMEM
-//                        through cp.async.bulk (TMA 1D) into a STAGES-deep ring
-//                        completed on mbarriers; each thread reads its record
-//                        from SMEM (72-B stride: conflict-free per half-warp),
-//                        computes invariants -> eigenvalues in registers, and
-//                        the tile's outputs are staged in SMEM so the HBM
-//                        stores are contiguous 8-B-per-lane runs.
-//   k_advisory           deferred non_real_advisory: block-compacts the records
-//                        that k_fused marked pending (disc < 0) and evaluates
-//                        disc_tolerance only for them (bit-exact).
-//   k_triple_angle       batched triple_angle.
+//   k_fused<MODE,TMA,INV,FLAGS>  persistent eigvals / eigvalss kernel.  Work
+//       unit: a 64-record chunk (4608 B), two records per lane.  Each warp owns
+//       a 2-deep SMEM ring that lane 0 fills with cp.async.bulk (TMA 1D) on
+//       per-warp mbarriers -- no block barrier in the loop.  The record loop is
+//       software-pipelined: one step = eigenvalue stage of the previous record
+//       + invariants of the next, in one branch-free block (tier A); records
+//       outside the fast domain go to two out-of-line tiers chosen per warp.
+//       Outputs are stored straight from registers.
+//   k_invariants<TMA>            invariants only, same ring.
+//   k_advisory                   deferred non_real_advisory: block-compacts the
+//       records k_fused marked pending (disc < 0) and evaluates disc_tolerance
+//       only for them (bit-exact).
+//   k_triple_angle               batched triple_angle.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -89,35 +89,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         : "memory");
   } while (!done);
 }
-#ifndef EIG33_STREAM_HINTS
-#define EIG33_STREAM_HINTS 0
-#endif
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           unsigned long long* b) {
-#if EIG33_STREAM_HINTS
-  // input records are read exactly once: evict them from L2 first
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
-      "%2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(pol)
-      : "memory");
-#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(b))
       : "memory");
-#endif
-}
-// lambda / invariant stores: written once, never re-read by this kernel
-__device__ __forceinline__ void st_out(double* p, double v) {
-#if EIG33_STREAM_HINTS
-  __stcs(p, v);
-#else
-  *p = v;
-#endif
 }
 
 __device__ __forceinline__ void load_tables(double* tab) {
@@ -170,9 +148,6 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
 // Out-of-line tiers of the record pipeline.  Kept as real calls so that their
 // register demand never enters the allocation of the steady-state loop (an
 // inlined second tier made ptxas move arrays to local memory there and cost 3x).
-#ifndef EIG33_TIER_B_INLINE
-#define EIG33_TIER_B_INLINE __noinline__
-#endif
 struct M9 {
   double e[9];
 };
@@ -186,7 +161,7 @@ struct StepOut {
 // Tier B, warp-uniform: every lane moderate but some carried record has
 // j2 <= 0 or disc <= 0: branch-free eig_moderate_bl interleaved with the DAG.
 template <int MODE, bool WANT_FLAGS>
-__device__ EIG33_TIER_B_INLINE StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
+__device__ __noinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
   StepOut o;
   o.L = eig_moderate_bl(pc, tab);
   o.v = invariants_moderate(mm.e);
@@ -280,9 +255,7 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
   mod = is_moderate(m);
-#if EIG33_MODERATE_ZEROS
   if (!mod) mod = is_moderate_or_zero(m);
-#endif
 }
 template <bool TMA>
 __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
@@ -346,9 +319,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   auto store_lam = [&](const Lam& L) {
     if (!pvalid) return;
     EIG33_CHECK(pr >= 0 && pr < R.n);
-    st_out(lam + pr * 3 + 0, L.l1);
-    st_out(lam + pr * 3 + 1, L.l2);
-    st_out(lam + pr * 3 + 2, L.l3);
+    lam[pr * 3 + 0] = L.l1;
+    lam[pr * 3 + 1] = L.l2;
+    lam[pr * 3 + 2] = L.l3;
   };
   // One step of the record pipeline: stage 2 of the carried record, stage 1 of m.
   auto step = [&](long long r, bool valid) {
@@ -368,13 +341,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
-#if EIG33_EIG_FIRST
       L = eig_fast(pc, T.tab);
       v = invariants_moderate(m);
-#else
-      v = invariants_moderate(m);
-      L = eig_fast(pc, T.tab);
-#endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       if (MODE == kSym) f = 0;
       bad = false;

@@ -147,3 +147,28 @@ def test_moderate_tier_with_exact_zeros_is_bitwise():
     H.hm_eigvals_fast(U.ptr(a), U.S(n), U.ptr(lam))
     lam_r, _ = U.checker_eigvals(a, adv=False)
     assert (U.lam_error_units(lam, lam_r) <= U.TOL_UNITS).all()
+
+
+def test_transcendentals_misround_less_than_glibc():
+    """Against mpmath (160 bits): our restricted-domain atan2 / sin / cos are
+    correctly rounded on all but a tiny fraction of arguments, and misround
+    less often than the glibc routines the reference calls."""
+    mpmath.mp.prec = 160
+    rng = np.random.default_rng(77)
+    n = 8000
+    th = rng.uniform(0, 1.0471975511965979, n)
+    s, c, gs, gc = (np.empty(n) for _ in range(4))
+    U.hostmath().hm_sincos(U.ptr(th), U.S(n), U.ptr(s), U.ptr(c))
+    U.hostmath().hm_libm_sincos(U.ptr(th), U.S(n), U.ptr(gs), U.ptr(gc))
+    y = np.abs(rng.standard_normal(n)) * np.exp(rng.uniform(-5, 5, n))
+    x = rng.standard_normal(n) * np.exp(rng.uniform(-5, 5, n))
+    o, g = _atan2(y, x), _libm_atan2(y, x)
+    ours = theirs = 0
+    for i in range(n):
+        t = mpmath.mpf(th[i])
+        es, ec = float(mpmath.sin(t)), float(mpmath.cos(t))
+        ea = float(mpmath.atan2(mpmath.mpf(y[i]), mpmath.mpf(x[i])))
+        ours += (es != s[i]) + (ec != c[i]) + (ea != o[i])
+        theirs += (es != gs[i]) + (ec != gc[i]) + (ea != g[i])
+    assert ours <= 0.0005 * 3 * n
+    assert ours < theirs

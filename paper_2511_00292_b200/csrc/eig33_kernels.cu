@@ -471,7 +471,8 @@ __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict_
       double m[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
-      const Inv v = invariants(m);
+      const bool mod = is_moderate(m) || is_moderate_or_zero(m);
+      const Inv v = mod ? invariants_moderate(m) : invariants(m);  // same bits either way
       flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
     }
     __syncthreads();

@@ -1,0 +1,59 @@
+"""Property-based fuzzing (hypothesis) of the product arithmetic (CPU build of
+eig33_math.cuh, dispatching through the same tiers as the kernel) against the
+compiled reference core: arbitrary doubles -- NaN, +-inf, +-0, subnormals,
+huge/tiny exponents, exact ties -- must give bit-identical invariants and
+advisory flags, and eigenvalues within the north_star tolerance with the same
+non-finite classes."""
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from tests import _util as U
+
+pytestmark = pytest.mark.skipif(U.ref() is None, reason="compiled reference not built")
+
+special = st.sampled_from([0.0, -0.0, 1.0, -1.0, 0.5, 3.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324,
+                           2.2250738585072014e-308, 1.7976931348623157e308, 1e-300, 1e300, 2.0 ** -60,
+                           2.0 ** 60, 2.0 ** -61, 1.0 + 2.0 ** -52])
+anyfloat = st.floats(allow_nan=True, allow_infinity=True, width=64)
+moderate = st.floats(min_value=-4.0, max_value=4.0, allow_nan=False, width=64)
+entry = st.one_of(special, anyfloat, moderate, moderate.map(lambda x: round(x * 64) / 64))
+record = st.lists(entry, min_size=9, max_size=9)
+
+
+def _check(rows):
+    a = np.ascontiguousarray(np.array(rows, dtype=np.float64).reshape(-1, 9))
+    n = a.shape[0]
+    inv = np.empty((n, 4))
+    U.hostmath().hm_invariants(U.ptr(a), U.S(n), U.ptr(inv))
+    assert U.bit_equal(inv, U.checker_invariants(a)).all()
+    lam, adv = np.empty((n, 3)), np.empty(n, np.uint8)
+    U.hostmath().hm_eigvals(U.ptr(a), U.S(n), U.ptr(lam), U.ptr(adv))
+    lam_r, adv_r = U.checker_eigvals(a)
+    assert (adv == adv_r).all()
+    assert (U.lam_error_units(lam, lam_r) <= U.TOL_UNITS).all()
+    lam_f = np.empty((n, 3))
+    U.hostmath().hm_eigvals_fast(U.ptr(a), U.S(n), U.ptr(lam_f))  # tier-A path where eligible
+    assert (U.lam_error_units(lam_f, lam_r) <= U.TOL_UNITS).all()
+
+
+@settings(max_examples=400, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.lists(record, min_size=1, max_size=16))
+def test_fuzz_records_match_reference(rows):
+    _check(rows)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.lists(moderate.map(lambda x: round(x * 8) / 8), min_size=9, max_size=9),
+                min_size=1, max_size=16))
+def test_fuzz_grid_records_ties_and_cancellations(rows):
+    _check(rows)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(moderate, min_size=6, max_size=6), st.integers(-1074, 1023))
+def test_fuzz_scaled_symmetric(vals, k):
+    a = np.array([vals[0], vals[1], vals[2], vals[1], vals[3], vals[4], vals[2], vals[4], vals[5]])
+    with np.errstate(all="ignore"):
+        _check([np.ldexp(a, k)])

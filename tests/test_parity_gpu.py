@@ -448,3 +448,18 @@ def test_reference_eigensolver_known_answers():
     lam_s = eig.eigvalss(np.diag([1.0, 2.0, 3.0])).lam[0]
     assert np.abs(lam_s - [1, 2, 3]).max() <= 12 * 2.0 ** -53
     assert a.shape == (1, 9)
+
+
+def test_random_bit_patterns():
+    """Uniformly random 64-bit patterns as entries (NaN payloads, subnormals,
+    infinities, extreme exponents), alone and mixed row-wise with moderate
+    entries so warps straddle all three tiers."""
+    rng = np.random.default_rng(91)
+    n = 1 << 18
+    bits = rng.integers(0, 2 ** 63, size=(n, 9), dtype=np.int64) * rng.choice([1, -1], size=(n, 9))
+    a = bits.view(np.float64).copy()
+    mod = rng.standard_normal((n, 9))
+    pick = rng.random((n, 9)) < 0.7
+    a[n // 2:] = np.where(pick[n // 2:], mod[n // 2:], a[n // 2:])  # mostly-moderate rows
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, "random-bits")

@@ -463,3 +463,19 @@ def test_random_bit_patterns():
     a[n // 2:] = np.where(pick[n // 2:], mod[n // 2:], a[n // 2:])  # mostly-moderate rows
     lam, inv, flags = _run(a)
     _assert_parity(a, lam, inv, flags, "random-bits")
+
+
+def test_native_cxx_driver_runs(tmp_path):
+    """tools/native/eig33_bench.cpp: the C ABI driven from plain C++ (device
+    and host-buffer entry points agree)."""
+    exe = tmp_path / "eig33_bench"
+    so_dir = os.path.join(U.ROOT, "paper_2511_00292_b200")
+    r = subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(U.ROOT, "include"),
+                        os.path.join(U.ROOT, "tools", "native", "eig33_bench.cpp"),
+                        os.path.join(so_dir, "_eig33cuda.so"), "-Wl,-rpath," + so_dir,
+                        "-I/usr/local/cuda/include", "-L/usr/local/cuda/lib64", "-lcudart", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), "3", "18", "3"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "agree on record 0: yes" in out.stdout

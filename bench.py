@@ -19,6 +19,7 @@ import argparse
 import ctypes
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -96,6 +97,50 @@ def cpu_lib():
     if not os.path.exists(port):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
     return ctypes.CDLL(port), "port"
+
+
+def host_description():
+    """CPU model and C library of the host the CPU legs run on."""
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "libc": " ".join(platform.libc_ver()),
+            "host_threads": os.cpu_count()}
+
+
+def cpu_latency_ns(L, kind, iterations=1_000_000):
+    """The reference's own single-matrix latency discipline (src/bench.cpp:245-289):
+    eigvals_checksum_loop on generate_case(D2, U1, 1e-14), 10 timed blocks after a
+    warm-up block; returns (mean ns/eval, fastest ns/eval) or None for the port."""
+    if kind != "reference":
+        return None
+    import numpy as np
+
+    port = os.path.join(ROOT, "oracle", "liboracle.so")
+    if not os.path.exists(port):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
+    O = ctypes.CDLL(port)
+    O.orc_generate_case.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    d = np.array([1e-14])
+    m = np.empty(9)
+    O.orc_generate_case(1, 1, 1e-3, d.ctypes.data, 1, m.ctypes.data)  # D2 / U1 / delta 1e-14
+    L.ref_checksum_loop.restype = ctypes.c_uint64
+    L.ref_checksum_loop.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+    reps, per = 10, iterations // 10
+    L.ref_checksum_loop(m.ctypes.data, per // 10 + 1)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter_ns()
+        L.ref_checksum_loop(m.ctypes.data, per)
+        ts.append((time.perf_counter_ns() - t0) / per)
+    return statistics.mean(ts), min(ts)
 
 
 def cpu_eigvals_rate(a, seconds, threads):
@@ -240,6 +285,10 @@ def run_reference(args, rank, world):
         step()
     el = time.perf_counter() - t0
     v = sample * args.steps / el
+    lat = cpu_latency_ns(L, kind)
+    if lat is not None:
+        lat = {"mean": lat[0], "fastest": lat[1],
+               "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), 10 x 1e5 evals"}
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
@@ -249,7 +298,8 @@ def run_reference(args, rank, world):
                    "records_per_step": sample, "outputs": "lambda only"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{sample} config-3 records per step (numpy-generated, seed {SEED}), "
-                                   f"eig33::eigvals streamed over contiguous shards on {threads} threads"},
+                                   f"eig33::eigvals streamed over contiguous shards on {threads} threads",
+                         "latency_ns": lat, **host_description()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -421,9 +471,17 @@ def run_ours(args, rank, world, local_rank):
         a_host = a[:samp].cpu().numpy()
         threads = os.cpu_count() or 1
         rate, passes, kind = cpu_eigvals_rate(a_host, args.cpu_seconds, threads)
+        rate1, passes1, _ = cpu_eigvals_rate(a_host[: 1 << 20], min(args.cpu_seconds, 3.0), 1)
+        lat = cpu_latency_ns(*cpu_lib())
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"first {samp} records of this run's config-3 batch, {passes} timed passes "
-                         f"(~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads"}
+                         f"(~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads",
+               "one_core": {"value": rate1, "unit": UNIT,
+                            "sample": f"first {1 << 20} records, {passes1} passes on 1 thread"},
+               "latency_ns": None if lat is None else
+               {"mean": lat[0], "fastest": lat[1],
+                "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), 10 x 1e5 evals"},
+               **host_description()}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

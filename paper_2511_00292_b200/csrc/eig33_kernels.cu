@@ -34,6 +34,9 @@
 
 namespace eig33b {
 
+#ifndef EIG33_MEMONLY
+#define EIG33_MEMONLY 0
+#endif
 #ifndef EIG33_THREADS
 #define EIG33_THREADS 256
 #endif
@@ -341,8 +344,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
+#if EIG33_MEMONLY
+      // measurement build only: same data movement, no arithmetic
+      L = Lam{pc.a0, pc.a4, pc.a8};
+      v = Inv{m[0], 1.0, m[1], 1.0};
+#else
       L = eig_fast(pc, T.tab);
       v = invariants_moderate(m);
+#endif
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       if (MODE == kSym) f = 0;
       bad = false;

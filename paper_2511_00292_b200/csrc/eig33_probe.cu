@@ -125,3 +125,56 @@ extern "C" double eig33_probe_fp64_latency(int op, int chains, int warps) {
   if (op == 1) return chains == 1 ? lat_run<1, 1>(warps) : lat_run<4, 1>(warps);
   return chains == 1 ? lat_run<1, 2>(warps) : lat_run<4, 2>(warps);
 }
+
+// Sustained FP64 rate on data that keeps every datapath bit toggling: eight
+// independent chains of the chaotic map x <- x*x - 1.9999 (one DFMA each,
+// bounded in [-2, 2]).  Run for seconds this is the FP64 roof of a long,
+// power-capped step; a short run gives the burst rate.
+namespace {
+__global__ void __launch_bounds__(256) k_dfma_chaos(int iters, double* out) {
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = -1.5 + 3.0 * ((tid * 2654435761u + k * 40503u) & 0xFFFFu) / 65536.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], x[k], -1.9999);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace
+
+// DFMA thread-instructions per second over `seconds` of back-to-back launches.
+extern "C" double eig33_probe_fp64_chaos(double seconds) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out = nullptr;
+  if (cudaMalloc(&out, 64) != cudaSuccess) return -1.0;
+  const int blocks = sms * 8, threads = 256, iters = 8192;
+  k_dfma_chaos<<<blocks, threads>>>(iters, out);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  int reps = 0;
+  cudaEventRecord(e0);
+  while (ms < seconds * 1e3f) {
+    for (int r = 0; r < 8; ++r) k_dfma_chaos<<<blocks, threads>>>(iters, out);
+    reps += 8;
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess || ms <= 0) return -2.0;
+  return (double)reps * blocks * threads * (double)iters * 8.0 / (ms * 1e-3);
+}

@@ -21,3 +21,12 @@ for op, name in ((0, "DFMA"), (1, "DMUL"), (2, "DADD")):
         for w in (1, 4, 8, 16):
             cyc = L.eig33_probe_fp64_latency(op, ch, w)
             print(f"lat {name} chains={ch} warps/SM={w:2d}: {cyc:7.2f} cycles/iter -> {cyc/ch:6.2f} cyc/op/thread")
+L.eig33_probe_fp64_chaos.restype = ctypes.c_double
+L.eig33_probe_fp64_chaos.argtypes = [ctypes.c_double]
+for secs in (0.05, 3.0):
+    p = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.sw_power_cap",
+                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+    r = L.eig33_probe_fp64_chaos(secs)
+    p.terminate()
+    out = [l for l in p.stdout.read().strip().splitlines() if l.strip()]
+    print(f"chaotic DFMA {secs:4.2f} s: {r/1e12:6.2f} T/s   clocks/power tail {out[-3:]}")

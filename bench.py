@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=N_PER_GPU_DEFAULT, help="records per GPU")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-power-roof", action="store_true",
+                   help="skip the idle / stream / chaotic-FP64 power probes after the timed region")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -208,6 +210,19 @@ class Clocks:
     def mark_stop(self):
         self.t1 = time.time()
 
+    def window(self, t0, t1):
+        """Median (board W, SM MHz) of the samples taken in [t0, t1]."""
+        pw, sm = [], []
+        for ts, ln in list(self.lines):
+            f = [x.strip() for x in ln.split(",")]
+            if t0 <= ts <= t1 and len(f) >= 3:
+                try:
+                    sm.append(float(f[0]))
+                    pw.append(float(f[2]))
+                except ValueError:
+                    pass
+        return (statistics.median(pw) if pw else None, statistics.median(sm) if sm else None)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -239,6 +254,69 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "power_w_median": statistics.median(pw) if pw else None,
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def power_limit_w(dev):
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=power.limit",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=20).stdout.strip()
+        return float(out.splitlines()[0])
+    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+        return 1000.0
+
+
+def power_roof(L, clocks, pa, pl, n, st, stream, dev):
+    """Energy roof at the board power limit: measure, on this
+    GPU and this run's data, the idle draw, the energy per record of a plain
+    72 B-in / 24 B-out stream over the same buffers (eig33_probe_stream) and
+    the energy per FP64 instruction on chaotic operands (eig33_probe_fp64_chaos);
+    roof = (limit - idle) / (E_stream + ops_per_record * E_fp64)."""
+    import torch
+
+    if not clocks.proc:
+        return None
+    L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                     ctypes.c_void_p]
+    L.eig33_probe_fp64_chaos.restype = ctypes.c_double
+    L.eig33_probe_fp64_chaos.argtypes = [ctypes.c_double]
+    torch.cuda.synchronize()
+    t = time.time()
+    time.sleep(2.0)
+    p_idle, _ = clocks.window(t + 1.0, time.time())
+    # stream probe: ~2.5 s of back-to-back launches, events for the rate
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    L.eig33_probe_stream(pa, n, pl, st)
+    e0.record(stream)
+    t = time.time()
+    k = 0
+    while time.time() - t < 2.5:
+        L.eig33_probe_stream(pa, n, pl, st)
+        k += 1
+        if k % 16 == 0:
+            stream.synchronize()
+    e1.record(stream)
+    e1.synchronize()
+    rec_s = k * n / (e0.elapsed_time(e1) * 1e-3)
+    p_stream, mhz_stream = clocks.window(t + 1.0, time.time())
+    time.sleep(1.0)
+    t = time.time()
+    op_s = L.eig33_probe_fp64_chaos(2.5)
+    p_fp64, mhz_fp64 = clocks.window(t + 1.0, time.time())
+    if None in (p_idle, p_stream, p_fp64) or op_s <= 0:
+        return None
+    cap = power_limit_w(dev)
+    e_rec = (p_stream - p_idle) / rec_s
+    e_op = (p_fp64 - p_idle) / op_s
+    e_total = e_rec + FP64_OPS_PER_REC * e_op
+    return {"idle_w": p_idle, "limit_w": cap,
+            "stream": {"records_per_s": rec_s, "w": p_stream, "sm_mhz": mhz_stream,
+                       "nj_per_record": e_rec * 1e9},
+            "fp64_chaos": {"inst_per_s": op_s, "w": p_fp64, "sm_mhz": mhz_fp64,
+                           "pj_per_inst": e_op * 1e12},
+            "nj_per_record_model": e_total * 1e9,
+            "roof_records_per_s": (cap - p_idle) / e_total}
 
 
 def measured_peaks():
@@ -364,6 +442,7 @@ def run_ours(args, rank, world, local_rank):
     clocks.mark_stop()
     torch.cuda.synchronize()
     barrier()
+    proof = None if args.no_power_roof else power_roof(L, clocks, pa, pl, n, st, stream, dev)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -464,6 +543,10 @@ def run_ours(args, rank, world, local_rank):
         roofline["power"] = {"w_median": clk["power_w_median"], "cap_w": 1000.0,
                              "nj_per_record": clk["power_w_median"] / (value / world) * 1e9,
                              "sm_mhz_median": clk.get("sm_mhz")}
+        if proof:
+            roofline["power"]["cap_w"] = proof["limit_w"]
+            roofline["power"]["energy_roof"] = proof
+            roofline["power"]["frac"] = (value / world) / proof["roof_records_per_s"]
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only

@@ -257,8 +257,12 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
                                           bool& mod) {
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
+#if EIG33_MEMONLY == 2
+  mod = true;  // measurement build: no tier test either
+#else
   mod = is_moderate(m);
   if (!mod) mod = is_moderate_or_zero(m);
+#endif
 }
 template <bool TMA>
 __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,

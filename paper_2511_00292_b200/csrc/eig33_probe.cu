@@ -178,3 +178,24 @@ extern "C" double eig33_probe_fp64_chaos(double seconds) {
   if (cudaGetLastError() != cudaSuccess || ms <= 0) return -2.0;
   return (double)reps * blocks * threads * (double)iters * 8.0 / (ms * 1e-3);
 }
+
+// Pure stream with the kernel's traffic mix (72 B read, 24 B written per
+// record), no FP64: out[i] = a[3i] ^ a[3i+1] ^ a[3i+2] on the bit patterns.
+// Each warp load/store instruction covers 768 contiguous bytes.
+namespace {
+__global__ void __launch_bounds__(256) k_stream(const long long* __restrict__ a, long long n3,
+                                                long long* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n3; i += stride)
+    out[i] = __ldcs(a + 3 * i) ^ __ldcs(a + 3 * i + 1) ^ __ldcs(a + 3 * i + 2);
+}
+}  // namespace
+
+extern "C" int eig33_probe_stream(const double* a, long long n, double* lam, void* stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_stream<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const long long*>(a), n * 3,
+                                                       reinterpret_cast<long long*>(lam));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}

@@ -28,7 +28,10 @@ def test_const_division_is_ieee(c):
     tiny = np.ldexp(rng.random(1 << 16) + 1, rng.integers(-1074, -940, 1 << 16))
     specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
                          1.7976931348623157e308, -1.7976931348623157e308, 3.0, 27.0, 1.0])
-    x = np.concatenate([x, tiny, -tiny, specials])
+    # short mantissas: many exact quotients and quotients with few significant bits
+    short = np.ldexp(rng.integers(1, 1 << 20, n).astype(np.float64) * (1 - 2 * rng.integers(0, 2, n)),
+                     rng.integers(-960, 1000, n))
+    x = np.concatenate([x, tiny, -tiny, specials, short, 3.0 * short])
     q = _call_unary("hm_div", x, ctypes.c_int(c))
     assert U.bit_equal(q, x / c).all()
 

@@ -457,29 +457,54 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 }
 
 // Deferred advisory: evaluate src/eigensolver.cpp:54 only where k_fused found
-// disc < 0.  Each block compacts a 2048-record window of pending flags into
-// SMEM, then its threads work the compacted list densely.
-constexpr int kAdvWindow = 2048;
+// disc < 0.  A block takes a window of kThreads*16 records: each thread reads
+// its 16 flag bytes with one 16-B load, and a window with nothing pending is
+// dismissed by one __syncthreads_or (the common case costs one coalesced read
+// of the flags).  Otherwise the pending records are compacted into SMEM
+// (warp scan of per-thread counts) and the block works the list densely.
+constexpr int kAdvWindow = kThreads * 16;
 __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict__ a, long long n,
                                                        uint8_t* __restrict__ flags) {
   __shared__ int list[kAdvWindow];
-  __shared__ int count;
+  __shared__ int wsum[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = ((uintptr_t)flags & 15u) == 0;
+  constexpr uint64_t kPend8 = 0x0101010101010101ull * kPending;
   for (long long w0 = (long long)blockIdx.x * kAdvWindow; w0 < n;
        w0 += (long long)gridDim.x * kAdvWindow) {
-    if (threadIdx.x == 0) count = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < kAdvWindow; i += blockDim.x) {
-      const long long idx = w0 + i;
-      const bool pend = idx < n && (flags[idx] & kPending);
-      const unsigned ballot = __ballot_sync(0xffffffffu, pend);
-      int base = 0;
-      if ((threadIdx.x & 31) == 0 && ballot) base = atomicAdd(&count, __popc(ballot));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (pend) list[base + __popc(ballot & ((1u << (threadIdx.x & 31)) - 1u))] = i;
+    const long long base = w0 + 16LL * threadIdx.x;
+    uint64_t w[2] = {0, 0};
+    if (vec && base + 16 <= n) {
+      const ulonglong2 v2 = __ldcg(reinterpret_cast<const ulonglong2*>(flags + base));
+      w[0] = v2.x;
+      w[1] = v2.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (base + k < n) w[k >> 3] |= (uint64_t)flags[base + k] << (8 * (k & 7));
     }
+    const uint64_t pm0 = w[0] & kPend8, pm1 = w[1] & kPend8;
+    if (!__syncthreads_or((pm0 | pm1) != 0)) continue;
+    const int cnt = __popcll(pm0) + __popcll(pm1);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    const int c = count;
-    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    int pos = incl - cnt, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const int sw = wsum[w];
+      pos += w < warp ? sw : 0;
+      total += sw;
+    }
+    for (uint64_t r = pm0; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + ((__ffsll((long long)r) - 1) >> 3);
+    for (uint64_t r = pm1; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + 8 + ((__ffsll((long long)r) - 1) >> 3);
+    __syncthreads();
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
       const long long idx = w0 + list[j];
       double m[9];
 #pragma unroll
@@ -488,7 +513,7 @@ __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict_
       const Inv v = mod ? invariants_moderate(m) : invariants(m);  // same bits either way
       flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
     }
-    __syncthreads();
+    __syncthreads();  // list and wsum are reused by the next window
   }
 }
 
@@ -595,7 +620,7 @@ static int launch_advisory(const double* a, size_t n, uint8_t* flags, cudaStream
   int sms = (dev >= 0 && dev < 64) ? g_dev[dev].sms.load() : 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long windows = (long long)((n + kAdvWindow - 1) / kAdvWindow);
-  const long long grid = windows < 4LL * sms ? windows : 4LL * sms;
+  const long long grid = windows < 8LL * sms ? windows : 8LL * sms;
   k_advisory<<<(unsigned)grid, kThreads, 0, st>>>(a, (long long)n, flags);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_advisory launch", e);

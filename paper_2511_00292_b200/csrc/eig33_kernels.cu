@@ -48,6 +48,9 @@ namespace eig33b {
 #ifndef EIG33_MEMONLY
 #define EIG33_MEMONLY 0
 #endif
+#ifndef EIG33_PDL
+#define EIG33_PDL 1
+#endif
 #ifndef EIG33_THREADS
 #define EIG33_THREADS 256
 #endif
@@ -110,6 +113,24 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(b))
       : "memory");
+}
+
+// Programmatic dependent launch: k_fused / k_invariants are launched with
+// programmatic stream serialisation, so their blocks may start while the
+// previous kernel on the stream drains.  Everything before pdl_wait() touches
+// only SMEM (barrier init, table copy from a read-only global array); every
+// read or write of caller buffers comes after it, and griddepcontrol.wait
+// returns only once the previous grid has completed and its writes are
+// visible.  pdl_trigger() lets the next kernel do the same.
+__device__ __forceinline__ void pdl_trigger() {
+#if EIG33_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if EIG33_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 }
 
 __device__ __forceinline__ void load_tables(double* tab) {
@@ -318,8 +339,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   load_tables(S.tab);
   __syncthreads();  // tables + barrier init; the only block-wide barrier
+  pdl_wait();
   const Tabs T{S.tab};
   ring_prologue<TMA>(R, gw);
   if (gw >= R.nchunks) return;
@@ -450,7 +473,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();
   ring_prologue<TMA>(R, gw);
   uint32_t it = 0;
   for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
@@ -607,7 +632,22 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   const long long nblk = (nchunks + kWarps - 1) / kWarps;  // at least one chunk per warp
   const long long cap = (long long)d.sms.load() * occ;
   const long long grid = nblk < cap ? nblk : cap;
+#if EIG33_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a, (long long)n, inv, lam, flags);
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_fused launch", e);
+#else
   kern<<<(unsigned)grid, kThreads, smem, st>>>(a, (long long)n, inv, lam, flags);
+#endif
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_fused launch", e);
   return EIG33_OK;

@@ -415,6 +415,45 @@ def test_concurrent_host_threads_and_streams():
         assert U.bit_equal(o.cpu().numpy(), want.lam).all()
 
 
+def test_dependent_launches_in_stream_order():
+    """k_fused / k_invariants start under programmatic dependent launch: their
+    prologue may overlap the previous kernel, but no caller buffer is touched
+    before griddepcontrol.wait.  Chain kernels where each one reads (RAW) or
+    overwrites (WAR) what the previous one wrote, with no host sync in between,
+    and compare with the same chain run one synchronised call at a time."""
+    n = 3 * (1 << 18)  # lam of n records = n/3 records of 9 doubles
+    a = eig.generate(3, n, seed=404)
+    L = eig.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+
+    def chain(sync):
+        lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        inv = torch.empty((n // 3, 4), dtype=torch.float64, device="cuda")
+        lam2 = torch.empty((n // 3, 3), dtype=torch.float64, device="cuda")
+        outs = []
+        for rep in range(3):
+            assert L.eig33cu_eigvals(P(a), n, None, P(lam), None, st) == 0          # writes lam
+            if sync:
+                torch.cuda.synchronize()
+            assert L.eig33cu_invariants(P(lam), n // 3, P(inv), st) == 0            # RAW on lam
+            if sync:
+                torch.cuda.synchronize()
+            assert L.eig33cu_eigvals(P(lam), n // 3, None, P(lam2), None, st) == 0  # RAW on lam
+            if sync:
+                torch.cuda.synchronize()
+            lam.fill_(float(rep))                                                   # WAR on lam
+            outs += [inv.clone(), lam2.clone()]
+        torch.cuda.synchronize()
+        return [o.cpu().numpy() for o in outs]
+
+    want = chain(True)
+    for _ in range(3):
+        got = chain(False)
+        for g, w in zip(got, want):
+            assert U.bit_equal(g, w).all()
+
+
 def test_generate_case_matches_port_bitwise():
     """Batched paper corpora (src/bench.cpp:53-82) on the device equal the C
     restatement bit for bit for every path x transform over the reference grid."""

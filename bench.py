@@ -256,6 +256,37 @@ class Clocks:
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def pcie_rates(torch, h_a, h_l, dev):
+    """Pinned-buffer copy rates (GB/s): H2D alone, D2H alone, H2D + D2H at once."""
+    src = h_a.view(-1)[: min(h_a.numel(), 1 << 27)]
+    out = h_l.view(-1)[: min(h_l.numel(), 1 << 27)]
+    d_in = torch.empty(src.numel(), dtype=src.dtype, device=dev)
+    d_out = torch.zeros(out.numel(), dtype=out.dtype, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(jobs, reps=3):
+        torch.cuda.synchronize(dev)
+        ev = []
+        for s, f, nbytes in jobs:
+            with torch.cuda.stream(s):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    f()
+                e1.record()
+                ev.append((e0, e1, nbytes))
+        torch.cuda.synchronize(dev)
+        return [reps * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9 for e0, e1, nb in ev]
+
+    h2d = (s1, lambda: d_in.copy_(src, non_blocking=True), src.numel() * 8)
+    d2h = (s2, lambda: out.copy_(d_out, non_blocking=True), out.numel() * 8)
+    timed([h2d], 1)
+    r = {"h2d_gbs": timed([h2d])[0], "d2h_gbs": timed([d2h])[0]}
+    r["h2d_concurrent_gbs"], r["d2h_concurrent_gbs"] = timed([h2d, d2h])
+    del d_in, d_out
+    return r
+
+
 def power_limit_w(dev):
     try:
         out = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=power.limit",
@@ -444,6 +475,9 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     proof = None if args.no_power_roof else power_roof(L, clocks, pa, pl, n, st, stream, dev)
     clk = clocks.stop()
+    if proof is not None:  # the stream probe wrote over lam: restore the step's result
+        step()
+        stream.synchronize()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -486,27 +520,28 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
         same = bool(torch.equal(h_l.view(torch.int64), lam[:ne].cpu().view(torch.int64)))
-        # PCIe roof for this path: plain pinned H2D copy bandwidth on this box
-        probe = h_a.view(-1)[: min(h_a.numel(), 1 << 28)]
-        dst = torch.empty(probe.numel(), dtype=probe.dtype, device=dev)
-        dst.copy_(probe, non_blocking=True)
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record()
-        for _ in range(3):
-            dst.copy_(probe, non_blocking=True)
-        c1.record()
-        c1.synchronize()
-        h2d_gbs = 3 * probe.numel() * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
-        del dst, probe
+        # PCIe roof for this path, measured on this box with the same pinned
+        # buffers: H2D alone, D2H alone, and both at once on two streams (the
+        # link is not fully duplex here: concurrent D2H slows H2D).
+        link = pcie_rates(torch, h_a, h_l, dev)
+        # duplex model: each record's 24 B of D2H runs alongside H2D at the
+        # concurrent rates, the rest of its 72 B of H2D at the solo rate.
+        t_rec = 24 / link["d2h_concurrent_gbs"] + \
+            max(0.0, 72 - link["h2d_concurrent_gbs"] * 24 / link["d2h_concurrent_gbs"]) / link["h2d_gbs"]
+        model = 1e9 / t_rec
         e2e_value = ne * world * args.e2e_steps / el
         e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * 72,
                "d2h_bytes_per_step": ne * 24, "steps": args.e2e_steps, "records_per_gpu_per_step": ne,
                "api": "eig33_eigvals_host (pinned host buffers, chunked H2D/kernel/D2H over 3 streams)",
                "bitwise_equal_to_device_path": same,
-               "pcie_roofline": {"bound": "pcie_h2d", "h2d_gbs_measured": h2d_gbs,
+               "pcie_roofline": {"bound": "pcie", "h2d_gbs_measured": link["h2d_gbs"],
+                                 "d2h_gbs_measured": link["d2h_gbs"],
+                                 "concurrent_h2d_gbs": link["h2d_concurrent_gbs"],
+                                 "concurrent_d2h_gbs": link["d2h_concurrent_gbs"],
                                  "achieved_h2d_gbs": e2e_value / world * 72 / 1e9,
-                                 "frac": e2e_value / world * 72 / 1e9 / h2d_gbs}}
+                                 "h2d_only_roof_records_per_s": link["h2d_gbs"] * 1e9 / 72,
+                                 "duplex_model_records_per_s": model,
+                                 "frac": e2e_value / world / model}}
         del h_a, h_l
 
     if rank != 0:

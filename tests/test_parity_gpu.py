@@ -230,6 +230,20 @@ def test_host_entry_points_equal_device_entry_points():
     assert U.bit_equal(eig.invariants(a), r_h.inv).all()
 
 
+def test_host_pipeline_reuses_staging_sets():
+    """Host-buffer API over more chunks than staging sets (7 x 2^22 + 3 records,
+    3 sets): every chunk's kernel must see its own H2D copy, never a stale
+    buffer, with the kernels launched under programmatic dependent launch."""
+    n = 7 * (1 << 22) + 3
+    a_d = eig.generate(3, n, seed=77)
+    want = eig.eigvals(a_d).lam.cpu().numpy()
+    a = a_d.cpu().numpy()
+    del a_d
+    for _ in range(2):
+        got = eig.eigvals(a).lam
+        assert U.bit_equal(got, want).all()
+
+
 def test_shard_invariance_bitwise():
     """Results are identical whatever the contiguous even-aligned sharding
     (the multi-GPU driver's partition), emulated on one device."""

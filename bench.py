@@ -146,8 +146,8 @@ def cpu_latency_ns(L, kind, iterations=1_000_000):
 
 
 def cpu_eigvals_rate(a, seconds, threads):
-    """Stream eigvals over the host sample `a` repeatedly for ~`seconds`;
-    returns (matrices/s, passes)."""
+    """Stream eigvals over the host sample `a` repeatedly for ~`seconds` (>= 5
+    passes after one warm-up pass); returns (median-pass matrices/s, passes, kind)."""
     import numpy as np
 
     L, kind = cpu_lib()
@@ -163,14 +163,17 @@ def cpu_eigvals_rate(a, seconds, threads):
 
     one()  # warm-up pass
     t0 = time.perf_counter()
-    passes = 0
+    ts = []
     while True:
+        t1 = time.perf_counter()
         one()
-        passes += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
+        ts.append(time.perf_counter() - t1)
+        if time.perf_counter() - t0 >= seconds and len(ts) >= 5:
             break
-    return n * passes / el, passes, kind
+    # median pass (best/median of >= 5 passes); best in cpu_pass_stats
+    cpu_eigvals_rate.last = {"passes": len(ts), "median": n / statistics.median(ts),
+                             "best": n / min(ts), "mean": n * len(ts) / sum(ts)}
+    return n / statistics.median(ts), len(ts), kind
 
 
 # ---------------------------------------------------------------------------
@@ -589,11 +592,14 @@ def run_ours(args, rank, world, local_rank):
         a_host = a[:samp].cpu().numpy()
         threads = os.cpu_count() or 1
         rate, passes, kind = cpu_eigvals_rate(a_host, args.cpu_seconds, threads)
+        stats = dict(cpu_eigvals_rate.last)
         rate1, passes1, _ = cpu_eigvals_rate(a_host[: 1 << 20], min(args.cpu_seconds, 3.0), 1)
         lat = cpu_latency_ns(*cpu_lib())
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"first {samp} records of this run's config-3 batch, {passes} timed passes "
-                         f"(~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads",
+               "sample": f"first {samp} records of this run's config-3 batch, median of {passes} timed "
+                         f"passes (~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads "
+                         f"(contiguous shards, one thread pinned per core)",
+               "passes": stats,
                "one_core": {"value": rate1, "unit": UNIT,
                             "sample": f"first {1 << 20} records, {passes1} passes on 1 thread"},
                "latency_ns": None if lat is None else

@@ -11,6 +11,9 @@
 //   eig33::eigvalss(const Mat3&)                      include/eig33/eigensolver.hpp:45
 //   eig33::triple_angle(double, double)               include/eig33/eigensolver.hpp:21
 //   eig33::eigvals_checksum_loop(const Mat3&, n)      include/eig33/eigensolver.hpp:57
+#include <pthread.h>
+#include <sched.h>
+
 #include <cstdint>
 #include <cstring>
 #include <thread>
@@ -28,17 +31,36 @@ eig33::Mat3 load(const double* p) {
   return m;
 }
 
+// CPUs this process may run on, in order (the baseline pins thread t to the
+// t-th of them: contiguous shards, one pinned thread per core).
+std::vector<int> allowed_cpus() {
+  std::vector<int> cpus;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  if (sched_getaffinity(0, sizeof set, &set) == 0)
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &set)) cpus.push_back(c);
+  return cpus;
+}
+
 template <class F>
 void parallel_shards(std::size_t n, int nthreads, F&& body) {
   if (nthreads <= 1 || n < 2) {
     body(std::size_t{0}, n);
     return;
   }
+  static const std::vector<int> cpus = allowed_cpus();
   std::vector<std::thread> pool;
   pool.reserve(nthreads);
   for (int t = 0; t < nthreads; ++t) {
     const std::size_t lo = n * t / nthreads, hi = n * (t + 1) / nthreads;
     pool.emplace_back([&body, lo, hi] { body(lo, hi); });
+    if (!cpus.empty()) {
+      cpu_set_t one;
+      CPU_ZERO(&one);
+      CPU_SET(cpus[t % cpus.size()], &one);
+      pthread_setaffinity_np(pool.back().native_handle(), sizeof one, &one);
+    }
   }
   for (auto& th : pool) th.join();
 }

@@ -149,7 +149,7 @@ struct Tabs {
 };
 
 // Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
-// the eigen-stage carry.  Moderate records (every |a_ij| in [2^-60,2^60), the
+// the eigen-stage carry.  Moderate records (every |a_ij| in [2^-100,2^100), the
 // common case) use the CSE DAG; the rest the checked reference-order kernel.
 // Both produce the reference's bits.
 template <int MODE, bool WANT_FLAGS>

@@ -1,7 +1,7 @@
 """Generate eig33_inv_dag.h: the reference's stable invariant kernels
 (/root/reference/proj/src/invariants_impl.hpp:21-85) as an explicit
 common-subexpression DAG, for records whose entries all lie in
-[2^-60, 2^60) in magnitude (the kernel's "moderate" fast path).
+[2^-100, 2^100) in magnitude (the kernel's "moderate" fast path).
 
 Every rounded operation of the reference is computed exactly once with the
 same operands, up to these value-preserving identities of IEEE binary64
@@ -11,7 +11,8 @@ round-to-nearest:
   (3) a + (-b) == a - b and a - (-b) == a + b   (IEEE defines subtraction so);
   (4) fl(fl(w*u)*v) == w*fl(u*v) and fl(acc + w*p) == fma(w, p, acc) for
       w in {2, 8} when no intermediate overflows or is subnormal -- which the
-      moderate range guarantees (every nonzero degree-6 product is >= 2^-672).
+      moderate range guarantees (every nonzero degree-6 product is a multiple
+      of 2^-912 and below ~2^620; see is_moderate in eig33_math.cuh).
 Identities that are NOT value-preserving (e.g. -(a+b) == (-a)+(-b), wrong for
 exact cancellation to zero) are not used.  Bit-exactness is checked against the
 compiled reference in tests/test_hostmath.py and tests/test_parity_gpu.py.
@@ -168,7 +169,7 @@ def main():
     hdr = f"""// Generated by gen_inv_dag.py -- do not edit.
 // Stable invariants of /root/reference/proj/src/invariants_impl.hpp:21-85 as an
 // explicit CSE DAG ({total} binary64 operations: {counts}).
-// Valid only for records with every |a_ij| in [2^-60, 2^60) (see gen_inv_dag.py).
+// Valid only for records with every |a_ij| in [2^-100, 2^100) (see gen_inv_dag.py).
 #pragma once
 
 EIG33_HD Inv invariants_moderate(const double a[9]) {{

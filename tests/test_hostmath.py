@@ -152,6 +152,60 @@ def test_moderate_tier_with_exact_zeros_is_bitwise():
     assert (U.lam_error_units(lam, lam_r) <= U.TOL_UNITS).all()
 
 
+def _moderate_edge_corpus(n, seed):
+    """Records at the edges of the moderate range [2^-100, 2^100): grid records
+    (ties, exact cancellations, repeated eigenvalues) scaled to sit just inside
+    either end, and near-scalar records c*I + d*E with off-diagonals down to
+    ~2^-99 (differences and products land on the finest grains the range allows)."""
+    rng = np.random.default_rng(seed)
+    k = n // 4
+    g = np.round(rng.uniform(-8, 8, (2 * k, 9)) * 64) / 64          # multiples of 2^-6, |.| <= 8
+    g[g == 0] = 2.0 ** -6
+    lo = g[:k] * 2.0 ** rng.integers(-93, -88, (k, 1))                # entries in [2^-99, 2^-85]
+    hi = g[k:] * 2.0 ** rng.integers(88, 96, (k, 1))                  # entries in [2^82, 2^99]
+    c = rng.uniform(-1, 1, (k, 1))
+    d = 2.0 ** rng.uniform(-97, -60, (k, 1))
+    e = rng.standard_normal((k, 9))
+    e = np.where(np.abs(e) < 2.0 ** -2, 2.0 ** -2, e)
+    ns = d * e
+    ns[:, [0, 4, 8]] += c
+    sym = ns.copy()
+    sym[:, [3, 6, 7]] = sym[:, [1, 2, 5]]
+    # finest grains: diagonals 2^-100 * (1 + i*2^-52) (differences of 2^-152),
+    # off-diagonals 0 or +-2^-100 * small integers, and the mirror image at 2^99
+    m = 4096
+    x = 2.0 ** -100
+    fine = np.zeros((m, 9))
+    fine[:, 0] = x * (1 + rng.integers(0, 4, m) * 2.0 ** -52)
+    fine[:, 4] = x * (1 + rng.integers(0, 4, m) * 2.0 ** -52)
+    fine[:, 8] = x * (1 + rng.integers(0, 4, m) * 2.0 ** -52)
+    off = rng.integers(-2, 3, (m, 6)) * x
+    fine[:, [1, 2, 3, 5, 6, 7]] = off
+    big = fine * 2.0 ** 198
+    return np.ascontiguousarray(np.concatenate([lo, hi, ns, sym, fine, big])[-n:])
+
+
+def test_widened_moderate_range_is_bitwise():
+    """The moderate tier (guard-free CSE invariants, two-op divisions,
+    guard-free eigenvalue stage) at the edges of [2^-100, 2^100) reproduces the
+    compiled reference: invariants bit for bit, lambda within the gate."""
+    a = _moderate_edge_corpus(1 << 18, 52)
+    H = U.hostmath()
+    ok = np.array([H.hm_is_moderate_or_zero(U.ptr(a[i])) for i in range(0, a.shape[0], 101)])
+    assert ok.all()
+    n = a.shape[0]
+    inv = np.empty((n, 4))
+    H.hm_invariants(U.ptr(a), U.S(n), U.ptr(inv))
+    assert U.bit_equal(inv, U.checker_invariants(a)).all()
+    lam = np.empty((n, 3))
+    H.hm_eigvals_fast(U.ptr(a), U.S(n), U.ptr(lam))
+    lam_r, _ = U.checker_eigvals(a, adv=False)
+    assert (U.lam_error_units(lam, lam_r) <= U.TOL_UNITS).all()
+    # just outside the range the records must take the checked path
+    out = a[:64] * 2.0 ** -20
+    assert not any(H.hm_is_moderate_or_zero(U.ptr(out[i])) for i in range(64))
+
+
 def test_transcendentals_misround_less_than_glibc():
     """Against mpmath (160 bits): our restricted-domain atan2 / sin / cos are
     correctly rounded on all but a tiny fraction of arguments, and misround

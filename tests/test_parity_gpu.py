@@ -164,6 +164,17 @@ def test_mixed_corpus_and_nonfinite_classes():
     _assert_parity(a, lam, inv, flags, "mixed")
 
 
+def test_moderate_range_edges():
+    """Records at both ends of the moderate tier's range [2^-100, 2^100) (finest
+    grains, near-scalar records with off-diagonals down to 2^-97, grid records
+    scaled to 2^+-90) take the guard-free tiers and reproduce the reference."""
+    from tests.test_hostmath import _moderate_edge_corpus
+
+    a = _moderate_edge_corpus(1 << 20, 53)
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, "moderate edges")
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 255, 256, 257, 511, 4097, 100003])
 def test_ragged_sizes_and_tails(n):
     a = U.mixed_corpus(max(n, 8), n)[:n]

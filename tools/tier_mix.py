@@ -1,6 +1,6 @@
 """Which k_fused tier each 32-record warp step of a BASELINE config takes:
 steady (all moderate, J2 > 0, disc > 0), moderate (all moderate, some J2 <= 0
-or disc <= 0) or general (some record outside [2^-60, 2^60) or non-finite)."""
+or disc <= 0) or general (some record outside [2^-100, 2^100) or non-finite)."""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np  # noqa: E402
@@ -12,7 +12,7 @@ for cfg in (1, 2, 3, 4, 5):
     inv = eig.invariants(a).cpu().numpy()
     h = a.cpu().numpy()
     e = (h.view(np.uint64) >> np.uint64(52)) & np.uint64(0x7FF)
-    ok = (h == 0) | ((e >= 1023 - 60) & (e < 1023 + 60))
+    ok = (h == 0) | ((e >= 1023 - 100) & (e < 1023 + 100))  # is_moderate: [2^-100, 2^100)
     mod = ok.all(axis=1)
     fast = mod & (inv[:, 1] > 0) & (inv[:, 3] > 0)
     w_mod = mod.reshape(-1, 32).all(axis=1)

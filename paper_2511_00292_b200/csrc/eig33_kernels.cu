@@ -148,6 +148,14 @@ struct Tabs {
   const double* tab;
 };
 
+// The checked reference-order kernels return the same bits as the moderate
+// ones on moderate records, so a warp with any non-moderate lane runs the
+// checked kernel on every lane rather than both kernels one after the other
+// (divergent lanes would serialise them).  `mask`: the lanes executing the call.
+__device__ __forceinline__ Inv invariants_warp(const double m[9], bool mod, unsigned mask) {
+  return __all_sync(mask, mod) ? invariants_moderate(m) : invariants(m);
+}
+
 // Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
 // the eigen-stage carry.  Moderate records (every |a_ij| in [2^-100,2^100), the
 // common case) use the CSE DAG; the rest the checked reference-order kernel.
@@ -167,7 +175,7 @@ __device__ __forceinline__ void stage1(double m[9], bool& mod, Inv& v, Carry& c,
     m[6] = m[2];
     m[7] = m[5];
   }
-  v = mod ? invariants_moderate(m) : invariants(m);
+  v = invariants_warp(m, mod, 0xffffffffu);
   if (MODE == kSym && bad) {
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     v.i1 = v.j2 = v.j3 = v.disc = qnan;
@@ -176,15 +184,22 @@ __device__ __forceinline__ void stage1(double m[9], bool& mod, Inv& v, Carry& c,
   c = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
 }
 
-// Stage 2 (eigenvalues) of a record from its carry, general form.
+// Stage 2 (eigenvalues) of a record from its carry, general form; called by
+// whole warps.  As in invariants_warp, the checked from_invariants serves every
+// lane once any lane needs it (same bits on moderate carries).
 __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const Tabs& T) {
+  Lam L;
+  if (__all_sync(0xffffffffu, mod || bad)) {
+    L = eig_moderate_bl(c, T.tab);
+  } else {
+    const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
+    L = from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
+  }
   if (bad) {
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-    return Lam{qnan, qnan, qnan};
+    L = Lam{qnan, qnan, qnan};
   }
-  if (mod) return eig_moderate_bl(c, T.tab);
-  const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
-  return from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
+  return L;
 }
 
 // Out-of-line tiers of the record pipeline.  Kept as real calls so that their
@@ -227,11 +242,11 @@ __device__ __noinline__ StepOut tier_general(M9 mm, bool sym_ok, bool mod, Carry
     o.bad = !sym_ok;  // already mirrored: the gate verdict decides
     o.f = o.bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
     o.mod = mod && !o.bad;
+    // rejected lanes do not vote: their (garbage) invariants are replaced by NaN
+    o.v = invariants_warp(mm.e, mod || o.bad, 0xffffffffu);
     if (o.bad) {
       const double qnan = __longlong_as_double(0x7ff8000000000000ll);
       o.v.i1 = o.v.j2 = o.v.j3 = o.v.disc = qnan;
-    } else {
-      o.v = mod ? invariants_moderate(mm.e) : invariants(mm.e);
     }
   } else {
     Carry nc;
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       bool mod;
       ring_read(buf, lane, h, m, mod);
       if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
-      const Inv v = mod ? invariants_moderate(m) : invariants(m);
+      const Inv v = invariants_warp(m, mod, 0xffffffffu);
       if (lane + 32 * h < cnt) {
         const long long r = c * kChunk + 32 * h + lane;
         inv[r * 4 + 0] = v.i1;
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict_
 #pragma unroll
       for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
       const bool mod = is_moderate(m) || is_moderate_or_zero(m);
-      const Inv v = mod ? invariants_moderate(m) : invariants(m);  // same bits either way
+      const Inv v = invariants_warp(m, mod, __activemask());  // same bits either way
       flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
     }
     __syncthreads();  // list and wsum are reused by the next window

@@ -368,6 +368,23 @@ def test_scaled_identities_exact():
     assert (lam == al[:, None]).all() and (inv[:, 1:] == 0).all() and not (flags & 1).any()
 
 
+def test_symmetric_disc_is_nonnegative():
+    """test_invariants.cpp:169-182 (500 matrices, U(-5,5), seed 23) at 2^20 records:
+    disc_stable of a bitwise-symmetric matrix is a sum of squares, so >= 0, and
+    no symmetric record raises the advisory; eigvalss equals eigvals there."""
+    rng = np.random.default_rng(23)
+    n = 1 << 20
+    a = rng.uniform(-5, 5, (n, 9))
+    a[:, [3, 6, 7]] = a[:, [1, 2, 5]]
+    lam, inv, flags = _run(a)
+    _assert_parity(a, lam, inv, flags, "symmetric U(-5,5)")
+    assert (inv[:, 3] >= 0.0).all()
+    assert not (flags & 1).any()
+    rs = eig.eigvalss(_dev(a), return_flags=True)
+    assert U.bit_equal(rs.lam.cpu().numpy(), lam).all()
+    assert not (rs.flags.cpu().numpy() & 2).any()
+
+
 def test_shift_equivariance():
     """test_eigensolver.cpp:104-128: entries and shifts on a 2^-20 grid, worst
     |(l(A)+beta) - l(A+beta I)| / (eps*(|beta| + ||A||_F)) <= 30."""

@@ -525,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // (warp scan of per-thread counts) and the block works the list densely.
 constexpr int kAdvWindow = kThreads * 16;
 __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict__ a, long long n,
+                                                       const double* __restrict__ inv,
                                                        uint8_t* __restrict__ flags) {
   __shared__ int list[kAdvWindow];
   __shared__ int wsum[kWarps];
@@ -570,8 +571,13 @@ __global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict_
       double m[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
-      const bool mod = is_moderate(m) || is_moderate_or_zero(m);
-      const Inv v = invariants_warp(m, mod, __activemask());  // same bits either way
+      Inv v;
+      if (inv) {  // k_fused already wrote this record's invariants
+        v = Inv{inv[idx * 4], inv[idx * 4 + 1], inv[idx * 4 + 2], inv[idx * 4 + 3]};
+      } else {
+        const bool mod = is_moderate(m) || is_moderate_or_zero(m);
+        v = invariants_warp(m, mod, __activemask());  // same bits either way
+      }
       flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
     }
     __syncthreads();  // list and wsum are reused by the next window
@@ -690,14 +696,15 @@ static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t
                  : dispatch_out<MODE, false>(a, n, inv, lam, flags, st);
 }
 
-static int launch_advisory(const double* a, size_t n, uint8_t* flags, cudaStream_t st) {
+static int launch_advisory(const double* a, size_t n, const double* inv, uint8_t* flags,
+                           cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = (dev >= 0 && dev < 64) ? g_dev[dev].sms.load() : 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long windows = (long long)((n + kAdvWindow - 1) / kAdvWindow);
   const long long grid = windows < 8LL * sms ? windows : 8LL * sms;
-  k_advisory<<<(unsigned)grid, kThreads, 0, st>>>(a, (long long)n, flags);
+  k_advisory<<<(unsigned)grid, kThreads, 0, st>>>(a, (long long)n, inv, flags);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_advisory launch", e);
   return EIG33_OK;
@@ -725,7 +732,7 @@ int eig33cu_eigvals(const double* d_a, size_t n, double* d_inv, double* d_lam, u
   if (n == 0) return EIG33_OK;
   if (!d_a || !d_lam) return fail(EIG33_EINVAL, "eig33cu_eigvals: null pointer");
   int rc = dispatch<kEig>(d_a, n, d_inv, d_lam, d_flags, (cudaStream_t)stream);
-  if (rc == EIG33_OK && d_flags) rc = launch_advisory(d_a, n, d_flags, (cudaStream_t)stream);
+  if (rc == EIG33_OK && d_flags) rc = launch_advisory(d_a, n, d_inv, d_flags, (cudaStream_t)stream);
   return rc;
 }
 

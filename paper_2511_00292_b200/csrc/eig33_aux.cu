@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#define EIG33_TABLE_DECL static __constant__
+#define EIG33_TABLE_DECL static __device__ __align__(16)  // as in eig33_kernels.cu
 #include "eig33_tables.h"
 #include "eig33_math.cuh"
 #include "eig33_internal.h"
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_eig_naive(const double* __restrict__ a,
                                                    double* __restrict__ lam,
                                                    uint8_t* __restrict__ flags) {
   __shared__ __align__(16) double tab[EIG33_TAB_N + 7];
-  for (int i = threadIdx.x; i < EIG33_TAB_N; i += blockDim.x) tab[i] = eig33_tab[i];
+  copy_table(tab, eig33_tab);
   __syncthreads();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {

@@ -26,18 +26,11 @@
 #include <mutex>
 #include <string>
 
-#ifndef EIG33_TAB_GLOBAL
-#define EIG33_TAB_GLOBAL 1
-#endif
-#if EIG33_TAB_GLOBAL
-// In global memory, not __constant__: the per-block copy into SMEM reads 32
-// different addresses per warp instruction, which the constant cache would
-// serialise; from global they are coalesced 16-B loads (L2 hits after the
-// first block).
+// The table lives in global memory, not __constant__: the per-block copy into
+// SMEM reads 32 different addresses per warp instruction, which the constant
+// cache would serialise; from global they are coalesced 16-B loads (L2 hits
+// after the first block).  See copy_table() in eig33_math.cuh.
 #define EIG33_TABLE_DECL static __device__ __align__(16)
-#else
-#define EIG33_TABLE_DECL static __constant__
-#endif
 #include "eig33_tables.h"
 #include "eig33_math.cuh"
 #include "eig33_internal.h"
@@ -134,14 +127,7 @@ __device__ __forceinline__ void pdl_wait() {
 }
 
 __device__ __forceinline__ void load_tables(double* tab) {
-#if EIG33_TAB_GLOBAL
-  const double2* src = reinterpret_cast<const double2*>(eig33_tab);
-  double2* dst = reinterpret_cast<double2*>(tab);
-  for (int i = threadIdx.x; i < kTabDoubles / 2; i += blockDim.x) dst[i] = __ldg(src + i);
-  if ((kTabDoubles & 1) && threadIdx.x == 0) tab[kTabDoubles - 1] = eig33_tab[kTabDoubles - 1];
-#else
-  for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) tab[i] = eig33_tab[i];
-#endif
+  copy_table(tab, eig33_tab);
 }
 
 struct Tabs {

@@ -193,6 +193,13 @@ int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_la
   cudaError_t e = cudaGetDeviceCount(&have);
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDeviceCount", e);
   if (ngpu < 1 || ngpu > have) return fail(EIG33_EINVAL, "ngpu out of range");
+  // Page-lock the whole buffers once (portable: every device sees them pinned).
+  // Left to the per-device calls, shard boundaries that share a page would make
+  // all but the first registration fail and fall back to pageable copies.
+  const PinGuard pin_a(h_a, n * 9 * sizeof(double));
+  const PinGuard pin_l(h_lam, n * 3 * sizeof(double));
+  const PinGuard pin_i(h_inv, h_inv ? n * 4 * sizeof(double) : 0);
+  const PinGuard pin_f(h_flags, h_flags ? n : 0);
   std::vector<int> rcs(ngpu, 0);
   std::vector<std::string> errs(ngpu);
   std::vector<std::thread> th;

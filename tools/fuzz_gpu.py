@@ -45,6 +45,18 @@ def main():
             lam, inv, flags = run(a)
             _assert_parity(a, lam, inv, flags, f"batch {b} {name}",
                            lam_tol_fallback=_exact.within_reference_forward_error if name == "config4" else None)
+            # invariants-only entry point: same bits as the fused kernel's
+            inv2 = eig.invariants(torch.from_numpy(a).cuda()).cpu().numpy()
+            assert U.bit_equal(inv2, inv).all(), f"batch {b} {name}: invariants entry differs"
+            # eigvalss on the mirrored corpus: equals eigvals bit for bit, no rejects
+            s_ = a.copy()
+            s_[:, [3, 6, 7]] = s_[:, [1, 2, 5]]
+            rs = eig.eigvalss(torch.from_numpy(s_).cuda(), return_flags=True)
+            re = eig.eigvals(torch.from_numpy(s_).cuda())
+            fl = rs.flags.cpu().numpy()
+            ok = (fl & 2) == 0  # NaN/inf records may still fail the gate, as in the reference
+            assert U.bit_equal(rs.lam.cpu().numpy()[ok], re.lam.cpu().numpy()[ok]).all(), \
+                f"batch {b} {name}: eigvalss != eigvals on symmetric input"
             checked += a.shape[0]
         print(f"batch {b}: {len(corpora)} corpora x {n} records ok ({time.time() - t0:.0f} s)", flush=True)
     print(f"fuzz ok: {checked} records")

@@ -118,8 +118,8 @@ def _records_np(a) -> np.ndarray:
         a = a.detach().cpu().numpy()
     arr = np.asarray(a)
     if arr.dtype != np.float64:
-        if not np.issubdtype(arr.dtype, np.number):
-            raise ValueError("matrix entries must be numeric")
+        if not (np.issubdtype(arr.dtype, np.floating) or np.issubdtype(arr.dtype, np.integer)):
+            raise ValueError("matrix entries must be real numbers")
         arr = arr.astype(np.float64)
     if arr.ndim == 2 and arr.shape == (3, 3):
         arr = arr.reshape(1, 9)

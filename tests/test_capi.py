@@ -57,6 +57,16 @@ def test_shape_validation_mirrors_reference_to_mat(shape):
         eig._records_np(np.zeros(shape))
 
 
+def test_entry_dtype_rules():
+    """Real numeric host input is converted to float64 (the reference binding
+    takes Python floats); complex, string and object input raise ValueError."""
+    assert eig._records_np(np.arange(18, dtype=np.int32).reshape(2, 3, 3)).dtype == np.float64
+    assert eig._records_np(np.ones((1, 9), np.float32)).dtype == np.float64
+    for bad in (np.zeros((2, 3, 3), complex), np.array([["a"] * 9]), np.array([[None] * 9])):
+        with pytest.raises(ValueError):
+            eig._records_np(bad)
+
+
 @pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
 def test_cxx_header_compiles_against_reference_types():
     """Drop-in: with the reference's own headers on the include path, batch.hpp

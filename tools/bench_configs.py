@@ -1,7 +1,10 @@
 """Throughput of every entry point on every BASELINE config at its batch size
 (supplementary to bench.py, whose line is config 3 / lambda only).  CUDA-event
-timing, device-resident inputs, 20 timed launches after 3 warm-ups."""
-import ctypes, json, os, sys
+timing, device-resident inputs, 20 timed launches after 3 warm-ups, each
+measurement after 1 s idle so that the previous one's power-capped clocks do
+not carry over (short runs: these are burst rates, above the sustained
+power-capped rate of bench.py)."""
+import ctypes, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2511_00292_b200 as eig
@@ -12,6 +15,8 @@ P = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
 def timeit(fn, reps=20, warm=3):
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()

@@ -558,7 +558,14 @@ def run_ours(args, rank, world, local_rank):
     per_launch_s = ms_step * 1e-3
     hbm_ach = n * BYTES_PER_REC / per_launch_s / 1e9
     fp64_ach = n * FP64_OPS_PER_REC / per_launch_s / 1e12
-    fp64_peak = fp64_rate / 1e12 if fp64_rate > 0 else None
+    # The timed region is a long step (~3 s), so the denominator is the sustained
+    # FP64 rate: chaotic-operand DFMA over 2.5 s from the energy-roof probes (it
+    # never reaches the power cap); the 11 ms burst probe if those were skipped.
+    sustained = proof["fp64_chaos"]["inst_per_s"] if proof else 0.0
+    fp64_peak = (sustained if sustained > 0 else fp64_rate) / 1e12 if max(sustained, fp64_rate) > 0 else None
+    fp64_src = ("measured on this GPU: sustained DFMA rate, chaotic operands, 2.5 s "
+                "(eig33_probe_fp64_chaos)" if sustained > 0 else
+                "measured on this GPU: burst DFMA issue rate (eig33_probe_fp64_rate)")
     traffic, recs = ncu_traffic()
     traffic_per_launch = traffic * n / recs if traffic and recs else None
     hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
@@ -566,7 +573,7 @@ def run_ours(args, rank, world, local_rank):
            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks.get("hbm_gbs") else "fallback"}
     fp64 = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "T fp64-inst/s",
             "frac": fp64_ach / fp64_peak if fp64_peak else None,
-            "peak_source": "measured on this GPU: DFMA issue rate (eig33_probe_fp64_rate)",
+            "peak_source": fp64_src, "burst_peak": fp64_rate / 1e12,
             "ops_per_record": FP64_OPS_PER_REC}
     # the binding roof is the slower one (BASELINE north_star): the one with the higher frac
     binding = fp64 if (fp64["frac"] or 0) >= hbm["frac"] else hbm

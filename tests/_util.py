@@ -28,7 +28,11 @@ def ptr(x):
 def _ensure_built():
     # both rebuild only what is stale (make / build._stale), so an edit to the
     # oracle or to eig33_math.cuh is always what the tests load
-    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
+    # the compiled reference too, where its sources exist (this container; the
+    # GPU box has no /root/reference and uses the prebuilt oracle/_ref .so)
+    have_ref = os.path.isdir("/root/reference/proj/src")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "all" if have_ref else "port"],
+                   check=True)
     from paper_2511_00292_b200 import build
     build.build_hostmath()
 

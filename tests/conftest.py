@@ -22,3 +22,7 @@ def pytest_sessionstart(session):
         from paper_2511_00292_b200 import build
 
         build.build_product()
+    # the checkers too, before collection evaluates the "reference built?" skips
+    from tests import _util
+
+    _util._ensure_built()

@@ -496,6 +496,48 @@ def test_dependent_launches_in_stream_order():
             assert U.bit_equal(g, w).all()
 
 
+def test_cuda_graph_capture_and_replay():
+    """The device entry points can be captured in a CUDA graph (the fused
+    kernels' programmatic-launch edges included) and replayed: same bits as
+    eager calls, and replays see new input contents."""
+    n = (1 << 18) + 37
+    a = eig.generate(4, n, seed=515)
+    L = eig.lib()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    inv = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    fl = torch.empty((n,), dtype=torch.uint8, device="cuda")
+    lam2 = torch.empty((n // 3, 3), dtype=torch.float64, device="cuda")
+
+    def calls(st):
+        assert L.eig33cu_eigvals(P(a), n, P(inv), P(lam), P(fl), st) == 0
+        assert L.eig33cu_eigvals(P(lam), n // 3, None, P(lam2), None, st) == 0  # reads lam (RAW)
+
+    calls(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))  # eager warm-up
+    torch.cuda.synchronize()
+    want = [x.clone() for x in (lam, inv, fl, lam2)]
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for x in (lam, inv, fl, lam2):
+            x.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            calls(ctypes.c_void_p(s.cuda_stream))
+    g.replay()
+    torch.cuda.synchronize()
+    for x, w in zip((lam, inv, fl, lam2), want):
+        assert torch.equal(x.view(torch.uint8), w.view(torch.uint8))
+    b = eig.generate(5, n, seed=516)
+    a.copy_(b)  # new contents, same buffer: the replay must pick them up
+    g.replay()
+    torch.cuda.synchronize()
+    r = eig.eigvals(b, return_invariants=True, return_flags=True)
+    assert torch.equal(lam.view(torch.uint8), r.lam.view(torch.uint8))
+    assert torch.equal(inv.view(torch.uint8), r.inv.view(torch.uint8))
+    assert torch.equal(fl, r.flags)
+
+
 def test_generate_case_matches_port_bitwise():
     """Batched paper corpora (src/bench.cpp:53-82) on the device equal the C
     restatement bit for bit for every path x transform over the reference grid."""

@@ -79,6 +79,10 @@ int eig33cu_eigvals_naive(const double* d_a, size_t n, double* d_lam, uint8_t* d
                           void* stream);
 int eig33cu_jacobians(const double* d_a, size_t n, double* d_jj2, double* d_jj3, double* d_jdisc,
                       void* stream);
+/* eig33::disc_naive(double j2, double j3) (include/eig33/invariants.hpp:59, src/invariants.cpp:58)
+ * elementwise over n pairs: ((4 j2) j2) j2 - (27 j3) j3, bit-exact. */
+int eig33cu_disc_naive(const double* d_j2, const double* d_j3, size_t n, double* d_disc,
+                       void* stream);
 
 /* Synchronous host-buffer versions on one device (chunked, pipelined
  * H2D / kernel / D2H over 3 streams).  eig33_eigvalss_host returns

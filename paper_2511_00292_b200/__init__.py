@@ -45,7 +45,7 @@ C_ABI_SYMBOLS = (
     "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
     "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
     "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
-    "eig33cu_generate_case",
+    "eig33cu_generate_case", "eig33cu_disc_naive",
 )
 VARIANTS = {"Stable": 0, "Naive": 1, "NaiveTensor": 2}  # reference AlgorithmVariant
 
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         "eig33cu_invariants_variant": ([P, S, I, P, P], I),
         "eig33cu_eigvals_naive": ([P, S, P, P, P], I),
         "eig33cu_jacobians": ([P, S, P, P, P, P], I),
+        "eig33cu_disc_naive": ([P, P, S, P, P], I),
         "eig33cu_generate_case": ([I, I, ctypes.c_double, P, S, P, P], I),
     }
     for name, (args, res) in sig.items():
@@ -283,20 +284,43 @@ def jacobians(a, *, device=0):
     return tuple(o.cpu().numpy() for o in outs) if host else tuple(outs)
 
 
-def triple_angle(j3, disc):
-    """Batched ``eig33::triple_angle`` on CUDA float64 vectors (eigensolver.hpp:21)."""
+def _vec_cuda(x, device):
+    """1-D float64 CUDA view of x; host input is copied to cuda:device (then
+    the result goes back to the host as numpy)."""
     torch = _torch()
-    if not (_is_cuda_tensor(j3) and _is_cuda_tensor(disc)):
-        raise ValueError("triple_angle takes CUDA float64 tensors")
-    j3 = j3.reshape(-1).contiguous()
-    disc = disc.reshape(-1).contiguous()
-    if j3.shape != disc.shape or j3.dtype != torch.float64 or disc.dtype != torch.float64:
-        raise ValueError("j3 and disc must be float64 tensors of equal length")
-    phi = torch.empty_like(j3)
-    with torch.cuda.device(j3.device):
-        _check(lib().eig33cu_triple_angle(_ptr(j3), _ptr(disc), j3.numel(), _ptr(phi), _stream(j3)),
-               "triple_angle")
-    return phi
+    if _is_cuda_tensor(x):
+        if x.dtype != torch.float64:
+            raise ValueError("CUDA input must be float64")
+        return x.reshape(-1).contiguous(), False
+    arr = np.asarray(x)
+    if not (np.issubdtype(arr.dtype, np.floating) or np.issubdtype(arr.dtype, np.integer)):
+        raise ValueError("entries must be real numbers")
+    arr = np.ascontiguousarray(arr, dtype=np.float64).reshape(-1)
+    return torch.from_numpy(arr).to(f"cuda:{int(device)}"), True
+
+
+def _pairwise(entry, what, x, y, device):
+    torch = _torch()
+    xd, host = _vec_cuda(x, device)
+    yd, _ = _vec_cuda(y, xd.device.index)
+    if xd.shape != yd.shape:
+        raise ValueError(f"{what}: arguments must have equal length")
+    out = torch.empty_like(xd)
+    with torch.cuda.device(xd.device):
+        _check(getattr(lib(), entry)(_ptr(xd), _ptr(yd), xd.numel(), _ptr(out), _stream(xd)), what)
+    return out.cpu().numpy() if host else out
+
+
+def triple_angle(j3, disc, *, device=0):
+    """Batched ``eig33::triple_angle`` (eigensolver.hpp:21): phi for each
+    (j3, disc) pair; CUDA float64 tensors in -> tensor out, host arrays -> numpy."""
+    return _pairwise("eig33cu_triple_angle", "triple_angle", j3, disc, device)
+
+
+def disc_naive(j2, j3, *, device=0):
+    """Batched ``eig33::disc_naive(j2, j3)`` (invariants.hpp:59, src/invariants.cpp:58):
+    ((4 j2) j2) j2 - (27 j3) j3 for each pair, on the GPU."""
+    return _pairwise("eig33cu_disc_naive", "disc_naive", j2, j3, device)
 
 
 def generate(config: int, n: int, seed: int = 0, first_index: int = 0, device="cuda"):

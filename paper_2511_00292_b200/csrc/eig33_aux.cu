@@ -88,6 +88,15 @@ __global__ void __launch_bounds__(256) k_jacobians(const double* __restrict__ a,
   }
 }
 
+// disc_naive(j2, j3) = ((4 j2) j2) j2 - (27 j3) j3 (src/invariants.cpp:58), elementwise
+__global__ void __launch_bounds__(256) k_disc_naive(const double* __restrict__ j2,
+                                                    const double* __restrict__ j3, long long n,
+                                                    double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = disc_naive(j2[i], j3[i]);
+}
+
 static unsigned grid_for(size_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -148,6 +157,19 @@ int eig33cu_jacobians(const double* d_a, size_t n, double* d_jj2, double* d_jj3,
   aux::k_jacobians<<<aux::grid_for(n), 256, 0, (cudaStream_t)stream>>>(d_a, (long long)n, d_jj2,
                                                                       d_jj3, d_jdisc);
   return aux::done("k_jacobians launch");
+}
+
+int eig33cu_disc_naive(const double* d_j2, const double* d_j3, size_t n, double* d_disc,
+                       void* stream) {
+  set_error("");
+  if (n == 0) return EIG33_OK;
+  if (!d_j2 || !d_j3 || !d_disc) {
+    set_error("eig33cu_disc_naive: null pointer");
+    return EIG33_EINVAL;
+  }
+  aux::k_disc_naive<<<aux::grid_for(n), 256, 0, (cudaStream_t)stream>>>(d_j2, d_j3, (long long)n,
+                                                                       d_disc);
+  return aux::done("k_disc_naive launch");
 }
 
 }  // extern "C"

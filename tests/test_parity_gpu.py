@@ -255,6 +255,29 @@ def test_host_pipeline_reuses_staging_sets():
         assert U.bit_equal(got, want).all()
 
 
+def test_host_staged_path_all_outputs():
+    """Pageable host batches >= 8 MB take the pinned-bounce staged pipeline:
+    every output (lambda, invariants, flags; eigvalss rejects; invariants-only)
+    equals the device path, including a ragged last chunk."""
+    n = 3 * (1 << 20) + 333
+    a_d = eig.generate(4, n, seed=88)
+    a = a_d.cpu().numpy()
+    r_d = eig.eigvals(a_d, return_invariants=True, return_flags=True)
+    r_h = eig.eigvals(a, return_invariants=True, return_flags=True)
+    assert U.bit_equal(r_h.lam, r_d.lam.cpu().numpy()).all()
+    assert U.bit_equal(r_h.inv, r_d.inv.cpu().numpy()).all()
+    assert (r_h.flags == r_d.flags.cpu().numpy()).all()
+    assert U.bit_equal(eig.invariants(a), r_d.inv.cpu().numpy()).all()
+    s_ = a.copy()
+    s_[:, [3, 6, 7]] = s_[:, [1, 2, 5]]
+    rs_h = eig.eigvalss(s_, return_flags=True)
+    rs_d = eig.eigvalss(torch.from_numpy(s_).cuda(), return_flags=True)
+    assert U.bit_equal(rs_h.lam, rs_d.lam.cpu().numpy()).all()
+    s_[n - 2, 1] += 1.0  # one asymmetric record in the last chunk
+    with pytest.raises(ValueError):
+        eig.eigvalss(s_)
+
+
 def test_shard_invariance_bitwise():
     """Results are identical whatever the contiguous even-aligned sharding
     (the multi-GPU driver's partition), emulated on one device."""

@@ -108,7 +108,7 @@ int eig33cu_generate(int config, uint64_t seed, uint64_t first_index, size_t n, 
 
 /* The paper's accuracy-sweep corpora: record i = generate_case(path, transform,
  * d_deltas[i]) = (U * diag(low, 1, 1 + delta)) * inverse_adjugate(U)
- * (reference include/eig33/bench.hpp, src/bench.cpp:53-75), bit-identical to
+ * (reference include/eig33/bench.hpp:47, src/bench.cpp:53-75), bit-identical to
  * the reference.  path: 0 = D1, 1 = D2; kind: 0 = Symm, 1 = U1, 2 = U2 (gamma
  * must be nonzero, as make_transform requires). */
 int eig33cu_generate_case(int path, int kind, double gamma, const double* d_deltas, size_t n,

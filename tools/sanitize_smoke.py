@@ -29,6 +29,13 @@ eig.invariants(a, variant="Naive")
 eig.invariants(a, variant="NaiveTensor")
 eig.eigvals_naive(a, return_flags=True)
 eig.jacobians(a)
-eig.eigvals(a)  # host pipeline
+eig.eigvals(a)  # host pipeline (pageable, direct)
+eig.disc_naive(j3, torch.randn(1000, dtype=torch.float64, device="cuda"))
+big = U.mixed_corpus((1 << 17) + 7, 4)  # >= 8 MB pageable: staged pinned-bounce pipeline
+eig.eigvals(big, return_invariants=True, return_flags=True)
+eig.invariants(big)
+from paper_2511_00292_b200 import eig33  # noqa: E402
+eig33.eigvals([[2, 1, 0], [1, 3, -1], [0, -1, 4]])
+eig33.jacobian_disc([1, 2, 3, 4, 5, 6, 7, 8, 10])
 torch.cuda.synchronize()
 print("sanitize smoke ok")

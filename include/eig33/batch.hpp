@@ -16,8 +16,8 @@
 // Without the reference headers on the include path, layout-identical
 // stand-in types are declared (Mat3 = 72-B row-major record, mat3.hpp:24-28;
 // InvariantSet 40 B, invariants.hpp:20-26; EigenTriple 32 B, eigensolver.hpp:29-34).
-// Only the Stable variant runs on the GPU; Naive/NaiveTensor throw
-// std::invalid_argument (out of the hot-path scope).
+// All three AlgorithmVariants run on the GPU (Stable on the fused hot path,
+// Naive / NaiveTensor on the study kernels), bit-exact like the scalar calls.
 #pragma once
 
 #include <cstddef>
@@ -82,17 +82,16 @@ inline void eigvals_packed(const Mat3* a, std::size_t n, double* lam, double* in
 
 inline void invariants(const Mat3* a, std::size_t n, InvariantSet* out,
                        AlgorithmVariant v = AlgorithmVariant::Stable) {
-  if (v != AlgorithmVariant::Stable)
-    throw std::invalid_argument("batched invariants: only AlgorithmVariant::Stable runs on the GPU");
   std::vector<double> inv(n * 4);
-  batch_detail::check(eig33_invariants_host(reinterpret_cast<const double*>(a), n, inv.data(),
-                                            batch_detail::device()));
+  const int variant = v == AlgorithmVariant::Stable ? 0 : v == AlgorithmVariant::Naive ? 1 : 2;
+  batch_detail::check(eig33_invariants_variant_host(reinterpret_cast<const double*>(a), n, variant,
+                                                    inv.data(), batch_detail::device()));
   for (std::size_t i = 0; i < n; ++i) {
     out[i].i1 = inv[4 * i];
     out[i].j2 = inv[4 * i + 1];
     out[i].j3 = inv[4 * i + 2];
     out[i].disc = inv[4 * i + 3];
-    out[i].variant = AlgorithmVariant::Stable;
+    out[i].variant = v;
   }
 }
 

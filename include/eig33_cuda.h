@@ -88,6 +88,10 @@ int eig33cu_disc_naive(const double* d_j2, const double* d_j3, size_t n, double*
  * H2D / kernel / D2H over 3 streams).  eig33_eigvalss_host returns
  * EIG33_ENOTSYM if any matrix failed the symmetry gate (outputs still written). */
 int eig33_invariants_host(const double* h_a, size_t n, double* h_inv, int device);
+/* invariants(a, variant) over host buffers, variant 0 Stable, 1 Naive, 2 NaiveTensor
+ * (include/eig33/invariants.hpp:74, src/invariants.cpp:76-98). */
+int eig33_invariants_variant_host(const double* h_a, size_t n, int variant, double* h_inv,
+                                  int device);
 int eig33_eigvals_host(const double* h_a, size_t n, double* h_inv, double* h_lam,
                        uint8_t* h_flags, int device);
 int eig33_eigvalss_host(const double* h_a, size_t n, double* h_inv, double* h_lam,

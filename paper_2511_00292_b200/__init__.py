@@ -45,7 +45,7 @@ C_ABI_SYMBOLS = (
     "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
     "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
     "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
-    "eig33cu_generate_case", "eig33cu_disc_naive",
+    "eig33cu_generate_case", "eig33cu_disc_naive", "eig33_invariants_variant_host",
 )
 VARIANTS = {"Stable": 0, "Naive": 1, "NaiveTensor": 2}  # reference AlgorithmVariant
 
@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
         "eig33cu_eigvals_naive": ([P, S, P, P, P], I),
         "eig33cu_jacobians": ([P, S, P, P, P, P], I),
         "eig33cu_disc_naive": ([P, P, S, P, P], I),
+        "eig33_invariants_variant_host": ([P, S, I, P, I], I),
         "eig33cu_generate_case": ([I, I, ctypes.c_double, P, S, P, P], I),
     }
     for name, (args, res) in sig.items():
@@ -235,13 +236,19 @@ def invariants(a, *, variant="Stable", device=0):
     if variant not in VARIANTS:
         raise ValueError(f"unknown AlgorithmVariant {variant!r}")
     if variant != "Stable":
-        torch = _torch()
-        d, host = _to_cuda(a, device)
-        with torch.cuda.device(d.device):
-            out = torch.empty((d.shape[0], 4), dtype=torch.float64, device=d.device)
-            _check(lib().eig33cu_invariants_variant(_ptr(d), d.shape[0], VARIANTS[variant], _ptr(out),
-                                                    _stream(d)), "invariants")
-        return out.cpu().numpy() if host else out
+        if _is_cuda_tensor(a):
+            torch = _torch()
+            d = _records_cuda(a)
+            with torch.cuda.device(d.device):
+                out = torch.empty((d.shape[0], 4), dtype=torch.float64, device=d.device)
+                _check(lib().eig33cu_invariants_variant(_ptr(d), d.shape[0], VARIANTS[variant],
+                                                        _ptr(out), _stream(d)), "invariants")
+            return out
+        arr = _records_np(a)
+        out = np.empty((arr.shape[0], 4))
+        _check(lib().eig33_invariants_variant_host(_ptr(arr), arr.shape[0], VARIANTS[variant], _ptr(out),
+                                                   int(device)), "invariants")
+        return out
     L = lib()
     if _is_cuda_tensor(a):
         torch = _torch()

@@ -115,7 +115,9 @@ struct PinGuard {
   }
 };
 
-enum class Op { Inv, Eig, Sym };
+// Inv* write invariants only (Stable, Naive, NaiveTensor); Eig/Sym write lambda.
+enum class Op { Inv, InvNaive, InvTensor, Eig, Sym };
+bool inv_only(Op op) { return op == Op::Inv || op == Op::InvNaive || op == Op::InvTensor; }
 
 bool is_pinned(const void* p) {
   if (!p) return true;
@@ -247,6 +249,8 @@ int launch_op(Op op, const double* d_a, size_t cnt, double* d_inv, double* d_lam
               cudaStream_t st) {
   switch (op) {
     case Op::Inv: return eig33cu_invariants(d_a, cnt, d_inv, st);
+    case Op::InvNaive: return eig33cu_invariants_variant(d_a, cnt, 1, d_inv, st);
+    case Op::InvTensor: return eig33cu_invariants_variant(d_a, cnt, 2, d_inv, st);
     case Op::Eig: return eig33cu_eigvals(d_a, cnt, d_inv, d_lam, d_fl, st);
     case Op::Sym: return eig33cu_eigvalss(d_a, cnt, d_inv, d_lam, d_fl, st);
   }
@@ -272,7 +276,7 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
     const cudaError_t e = cudaEventSynchronize(h.done[b]);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "staged D2H", e);
     if (out_inv) pool.copy(h_inv + lo * 4, h.inv[b], cnt * 4 * sizeof(double));
-    if (op != Op::Inv) pool.copy(h_lam + lo * 3, h.lam[b], cnt * 3 * sizeof(double));
+    if (!inv_only(op)) pool.copy(h_lam + lo * 3, h.lam[b], cnt * 3 * sizeof(double));
     if (want_flags) std::memcpy(flags_out + lo, h.fl[b], cnt);
     return EIG33_OK;
   };
@@ -290,7 +294,7 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
     if (out_inv && (e = cudaMemcpyAsync(h.inv[b], s.inv[b], cnt * 4 * sizeof(double),
                                         cudaMemcpyDeviceToHost, st)) != cudaSuccess)
       return fail(EIG33_ECUDA, "D2H inv", e);
-    if (op != Op::Inv && (e = cudaMemcpyAsync(h.lam[b], s.lam[b], cnt * 3 * sizeof(double),
+    if (!inv_only(op) && (e = cudaMemcpyAsync(h.lam[b], s.lam[b], cnt * 3 * sizeof(double),
                                               cudaMemcpyDeviceToHost, st)) != cudaSuccess)
       return fail(EIG33_ECUDA, "D2H lam", e);
     if (want_flags && (e = cudaMemcpyAsync(h.fl[b], s.flags[b], cnt, cudaMemcpyDeviceToHost, st)) !=
@@ -348,17 +352,13 @@ int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam,
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "H2D", e);
     double* dinv = h_inv ? s.inv[b] : nullptr;
     uint8_t* dfl = want_flags ? s.flags[b] : nullptr;
-    switch (op) {
-      case Op::Inv: rc = eig33cu_invariants(s.a[b], cnt, s.inv[b], st); break;
-      case Op::Eig: rc = eig33cu_eigvals(s.a[b], cnt, dinv, s.lam[b], dfl, st); break;
-      case Op::Sym: rc = eig33cu_eigvalss(s.a[b], cnt, dinv, s.lam[b], dfl, st); break;
-    }
+    rc = launch_op(op, s.a[b], cnt, inv_only(op) ? s.inv[b] : dinv, s.lam[b], dfl, st);
     if (rc) return fail(rc, eig33cu_last_error());
-    if (h_inv || op == Op::Inv) {
+    if (h_inv || inv_only(op)) {
       e = cudaMemcpyAsync(h_inv + lo * 4, s.inv[b], cnt * 4 * sizeof(double), cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) return fail(EIG33_ECUDA, "D2H inv", e);
     }
-    if (op != Op::Inv) {
+    if (!inv_only(op)) {
       e = cudaMemcpyAsync(h_lam + lo * 3, s.lam[b], cnt * 3 * sizeof(double), cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) return fail(EIG33_ECUDA, "D2H lam", e);
       if (want_flags) {
@@ -387,6 +387,15 @@ int eig33_invariants_host(const double* h_a, size_t n, double* h_inv, int device
   eig33b::set_error("");
   if (n && (!h_a || !h_inv)) return fail(EIG33_EINVAL, "eig33_invariants_host: null pointer");
   return run_device(Op::Inv, h_a, n, h_inv, nullptr, nullptr, device, nullptr);
+}
+
+int eig33_invariants_variant_host(const double* h_a, size_t n, int variant, double* h_inv,
+                                  int device) {
+  eig33b::set_error("");
+  if (n && (!h_a || !h_inv)) return fail(EIG33_EINVAL, "eig33_invariants_variant_host: null pointer");
+  if (variant < 0 || variant > 2) return fail(EIG33_EINVAL, "eig33_invariants_variant_host: bad variant");
+  const Op op = variant == 0 ? Op::Inv : variant == 1 ? Op::InvNaive : Op::InvTensor;
+  return run_device(op, h_a, n, h_inv, nullptr, nullptr, device, nullptr);
 }
 
 int eig33_eigvals_host(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,

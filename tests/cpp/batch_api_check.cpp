@@ -26,6 +26,14 @@ int main() {
     threw = true;
   }
   ok = ok && threw;
+  // the study variants go through the same batched overload (invariants.hpp:74)
+  std::vector<eig33::InvariantSet> nv(3), tv(3);
+  eig33::invariants(a.data(), a.size(), nv.data(), eig33::AlgorithmVariant::Naive);
+  eig33::invariants(a.data(), a.size(), tv.data(), eig33::AlgorithmVariant::NaiveTensor);
+  ok = ok && nv[0].variant == eig33::AlgorithmVariant::Naive &&
+       tv[0].variant == eig33::AlgorithmVariant::NaiveTensor && nv[0].i1 == 2.0 &&
+       std::fabs(nv[0].j2 - 7.0 / 3.0) < 1e-14 && std::fabs(tv[0].j3 + 20.0 / 27.0) < 1e-14 &&
+       std::fabs(nv[0].disc - 36.0) < 1e-12;
   std::printf("%s\n", ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
 }

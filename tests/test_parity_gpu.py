@@ -311,6 +311,16 @@ def test_cxx_batch_api_links_and_runs(tmp_path):
     assert out.returncode == 0 and out.stdout.strip() == "OK", out.stdout + out.stderr
 
 
+def test_variant_invariants_host_entry_equals_device():
+    """eig33_invariants_variant_host (pageable direct, pageable staged) gives
+    the device entry's bits for all three variants."""
+    for n in (1000, (1 << 17) + 3):
+        a = U.mixed_corpus(n, 29)
+        d = torch.from_numpy(a).cuda()
+        for v in ("Stable", "Naive", "NaiveTensor"):
+            assert U.bit_equal(eig.invariants(a, variant=v), eig.invariants(d, variant=v).cpu().numpy()).all()
+
+
 def test_study_variants_on_device():
     """naive / tensor invariants, eigvals_naive (+advisory), Jacobians vs the
     compiled reference: bit-exact except eigvals_naive's lambda (tolerance)."""

@@ -10,13 +10,15 @@
 //       a 2-deep SMEM ring that lane 0 fills with cp.async.bulk (TMA 1D) on
 //       per-warp mbarriers -- no block barrier in the loop.  The record loop is
 //       software-pipelined: one step = eigenvalue stage of the previous record
-//       + invariants of the next, in one branch-free block (tier A); records
-//       outside the fast domain go to two out-of-line tiers chosen per warp.
-//       Outputs are stored straight from registers.
+//       + invariants of the next, in one branch-free block (tier A); warps
+//       with records outside that domain take the moderate tier (inlined) or
+//       the general tier (an out-of-line call), chosen per warp.  Launched with
+//       programmatic dependent launch.  Outputs are stored straight from
+//       registers.
 //   k_invariants<TMA>            invariants only, same ring.
-//   k_advisory                   deferred non_real_advisory: block-compacts the
-//       records k_fused marked pending (disc < 0) and evaluates disc_tolerance
-//       only for them (bit-exact).
+//   k_advisory                   deferred non_real_advisory: scans the flags of
+//       a window with 16-B loads, block-compacts the records k_fused marked
+//       pending (disc < 0) and evaluates disc_tolerance only for them (bit-exact).
 //   k_triple_angle               batched triple_angle.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -188,9 +190,10 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
   return L;
 }
 
-// Out-of-line tiers of the record pipeline.  Kept as real calls so that their
-// register demand never enters the allocation of the steady-state loop (an
-// inlined second tier made ptxas move arrays to local memory there and cost 3x).
+// Slow tiers of the record pipeline.  The general tier is a real call so that
+// its register demand never enters the allocation of the steady-state loop
+// (inlining it made ptxas move arrays to local memory there and cost 3x); the
+// moderate tier is small enough to inline.
 struct M9 {
   double e[9];
 };

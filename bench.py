@@ -302,49 +302,61 @@ def power_limit_w(dev):
 
 def power_roof(L, clocks, pa, pl, n, st, stream, dev):
     """Energy roof at the board power limit: measure, on this
-    GPU and this run's data, the idle draw, the energy per record of a plain
-    72 B-in / 24 B-out stream over the same buffers (eig33_probe_stream) and
-    the energy per FP64 instruction on chaotic operands (eig33_probe_fp64_chaos);
-    roof = (limit - idle) / (E_stream + ops_per_record * E_fp64)."""
+    GPU and this run's data, the idle draw, the energy per record of the
+    kernel's own data path with the arithmetic removed (eig33_probe_memonly:
+    TMA ring, tier tests, lambda stores), of a plain 72 B-in / 24 B-out stream
+    (eig33_probe_stream, for reference), and the energy per FP64 instruction
+    on chaotic operands (eig33_probe_fp64_chaos);
+    roof = (limit - idle) / (E_datapath + ops_per_record * E_fp64)."""
     import torch
 
     if not clocks.proc:
         return None
     L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
                                      ctypes.c_void_p]
+    L.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
     L.eig33_probe_fp64_chaos.restype = ctypes.c_double
     L.eig33_probe_fp64_chaos.argtypes = [ctypes.c_double]
     torch.cuda.synchronize()
     t = time.time()
     time.sleep(2.0)
     p_idle, _ = clocks.window(t + 1.0, time.time())
-    # stream probe: ~2.5 s of back-to-back launches, events for the rate
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    L.eig33_probe_stream(pa, n, pl, st)
-    e0.record(stream)
-    t = time.time()
-    k = 0
-    while time.time() - t < 2.5:
-        L.eig33_probe_stream(pa, n, pl, st)
-        k += 1
-        if k % 16 == 0:
-            stream.synchronize()
-    e1.record(stream)
-    e1.synchronize()
-    rec_s = k * n / (e0.elapsed_time(e1) * 1e-3)
-    p_stream, mhz_stream = clocks.window(t + 1.0, time.time())
+    def probe(fn, secs=2.5):
+        """~secs of back-to-back launches: (records/s by CUDA events, median W, MHz)."""
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        fn()
+        e0.record(stream)
+        t = time.time()
+        k = 0
+        while time.time() - t < secs:
+            fn()
+            k += 1
+            if k % 16 == 0:
+                stream.synchronize()
+        e1.record(stream)
+        e1.synchronize()
+        w, mhz = clocks.window(t + 1.0, time.time())
+        return k * n / (e0.elapsed_time(e1) * 1e-3), w, mhz
+
+    rec_s, p_stream, mhz_stream = probe(lambda: L.eig33_probe_stream(pa, n, pl, st))
+    time.sleep(1.0)
+    dp_s, p_dp, mhz_dp = probe(lambda: L.eig33_probe_memonly(pa, n, pl, st))
     time.sleep(1.0)
     t = time.time()
     op_s = L.eig33_probe_fp64_chaos(2.5)
     p_fp64, mhz_fp64 = clocks.window(t + 1.0, time.time())
-    if None in (p_idle, p_stream, p_fp64) or op_s <= 0:
+    if None in (p_idle, p_stream, p_dp, p_fp64) or op_s <= 0:
         return None
     cap = power_limit_w(dev)
     e_rec = (p_stream - p_idle) / rec_s
+    e_dp = (p_dp - p_idle) / dp_s
     e_op = (p_fp64 - p_idle) / op_s
-    e_total = e_rec + FP64_OPS_PER_REC * e_op
+    e_total = e_dp + FP64_OPS_PER_REC * e_op
     return {"idle_w": p_idle, "limit_w": cap,
+            "datapath": {"records_per_s": dp_s, "w": p_dp, "sm_mhz": mhz_dp, "nj_per_record": e_dp * 1e9,
+                         "probe": "eig33_probe_memonly: k_fused's TMA ring, tier tests and stores, "
+                                  "no arithmetic"},
             "stream": {"records_per_s": rec_s, "w": p_stream, "sm_mhz": mhz_stream,
                        "nj_per_record": e_rec * 1e9},
             "fp64_chaos": {"inst_per_s": op_s, "w": p_fp64, "sm_mhz": mhz_fp64,

@@ -40,9 +40,6 @@
 
 namespace eig33b {
 
-#ifndef EIG33_MEMONLY
-#define EIG33_MEMONLY 0
-#endif
 #ifndef EIG33_PDL
 #define EIG33_PDL 1
 #endif
@@ -303,12 +300,8 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
                                           bool& mod) {
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
-#if EIG33_MEMONLY == 2
-  mod = true;  // measurement build: no tier test either
-#else
   mod = is_moderate(m);
   if (!mod) mod = is_moderate_or_zero(m);
-#endif
 }
 template <bool TMA>
 __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
@@ -331,7 +324,10 @@ __device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uin
 // transcendental chain of one record overlaps the wide invariant DAG of the
 // next.  Outputs go straight from registers to HBM (a warp's lambda stores
 // cover one contiguous 768-B run; L2 merges the sectors).
-template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS>
+// MEMONLY (measurement probe eig33_probe_memonly only): the same ring, tier
+// tests and stores with the steady-state arithmetic removed -- the kernel's own
+// data-movement energy for the energy roof in bench.py.
+template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS, bool MEMONLY = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
             double* __restrict__ lam, uint8_t* __restrict__ flags) {
@@ -396,14 +392,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
       // the long transcendental chain is written first so the scheduler
       // starts it early and fills its latency with the invariant DAG.
-#if EIG33_MEMONLY
-      // measurement build only: same data movement, no arithmetic
-      L = Lam{pc.a0, pc.a4, pc.a8};
-      v = Inv{m[0], 1.0, m[1], 1.0};
-#else
-      L = eig_fast(pc, T.tab);
-      v = invariants_moderate(m);
-#endif
+      if constexpr (MEMONLY) {  // measurement probe: same data movement, no arithmetic
+        L = Lam{pc.a0, pc.a4, pc.a8};
+        v = Inv{m[0], 1.0, m[1], 1.0};
+      } else {
+        L = eig_fast(pc, T.tab);
+        v = invariants_moderate(m);
+      }
       if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
       if (MODE == kSym) f = 0;
       bad = false;
@@ -749,6 +744,30 @@ int eig33cu_triple_angle(const double* d_j3, const double* d_disc, size_t n, dou
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_triple_angle launch", e);
   return EIG33_OK;
+}
+
+// Measurement probe (not part of the batched API): k_fused's data path -- TMA
+// ring, tier tests, lambda stores -- with the arithmetic removed, over a
+// 16-B-aligned batch.  bench.py times it for the energy roof.
+int eig33_probe_memonly(const double* d_a, size_t n, double* d_lam, void* stream) {
+  g_err.clear();
+  if (n == 0) return EIG33_OK;
+  if (!d_a || !d_lam || ((uintptr_t)d_a & 15u)) return fail(EIG33_EINVAL, "eig33_probe_memonly: bad argument");
+  auto kern = k_fused<kEig, true, false, false, true>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  });
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long nchunks = (long long)((n + kChunk - 1) / kChunk);
+  const long long nblk = (nchunks + kWarps - 1) / kWarps;
+  const long long cap = (long long)sms * kMinBlocks;
+  kern<<<(unsigned)(nblk < cap ? nblk : cap), kThreads, sizeof(Smem), (cudaStream_t)stream>>>(
+      d_a, (long long)n, nullptr, d_lam, nullptr);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EIG33_OK : fail(EIG33_ECUDA, "eig33_probe_memonly launch", e);
 }
 
 }  // extern "C"

@@ -1,9 +1,9 @@
 """Power/clock of the eigvals kernel vs. data-movement-only probes.
 
   python tools/power_memonly.py                      # product kernel
-  TAG=memonly EIG33_SO=.../variants/memonly.so python tools/power_memonly.py
-                                                     # EIG33_MEMONLY=1 build: same
-                                                     # ring/stores, no arithmetic
+  TAG=memonly python tools/power_memonly.py         # eig33_probe_memonly: the same
+                                                     # ring / tier tests / stores,
+                                                     # no arithmetic
   TAG=stream python tools/power_memonly.py           # eig33_probe_stream: plain
                                                      # 72 B in / 24 B out stream
 
@@ -50,7 +50,10 @@ def main():
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     pa, pl = ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(lam.data_ptr())
     tag = os.environ.get("TAG", "product")
-    if tag == "stream":
+    if tag == "memonly":
+        L.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
+        clk, pw, r = sample(lambda: L.eig33_probe_memonly(pa, n, pl, st))
+    elif tag == "stream":
         L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
                                          ctypes.c_void_p]
         clk, pw, r = sample(lambda: L.eig33_probe_stream(pa, n, pl, st))

@@ -1,6 +1,6 @@
 """Config-3 throughput by output mix (lam / lam+inv / lam+inv+flags / inv only),
 burst timing (20 launches of 2^26 records after 3 warm-ups).  Run against a
-variant with EIG33_SO=... to compare builds (e.g. the EIG33_MEMONLY=1 build)."""
+variant with EIG33_SO=... to compare builds."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch  # noqa: E402

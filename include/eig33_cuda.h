@@ -103,6 +103,9 @@ int eig33_eigvalss_host(const double* h_a, size_t n, double* h_inv, double* h_la
  * bitwise identical for every ngpu. */
 int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_lam,
                         uint8_t* h_flags, int ngpu);
+int eig33_multi_invariants(const double* h_a, size_t n, double* h_inv, int ngpu);
+int eig33_multi_eigvalss(const double* h_a, size_t n, double* h_inv, double* h_lam,
+                         uint8_t* h_flags, int ngpu);
 
 /* Synthetic corpora of the benchmark configs (BASELINE.json configs[0..4]),
  * counter-based: record i depends only on (config, seed, first_index + i), so

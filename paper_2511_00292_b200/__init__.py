@@ -43,7 +43,8 @@ EIG33_OK, EIG33_ECUDA, EIG33_EINVAL, EIG33_ENOTSYM = 0, 1, 2, 3
 C_ABI_SYMBOLS = (
     "eig33cu_version", "eig33cu_last_error", "eig33cu_invariants", "eig33cu_eigvals",
     "eig33cu_eigvalss", "eig33cu_triple_angle", "eig33_invariants_host", "eig33_eigvals_host",
-    "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33cu_generate",
+    "eig33_eigvalss_host", "eig33_multi_eigvals", "eig33_multi_invariants", "eig33_multi_eigvalss",
+    "eig33cu_generate",
     "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
     "eig33cu_generate_case", "eig33cu_disc_naive", "eig33_invariants_variant_host",
 )
@@ -74,6 +75,8 @@ def lib() -> ctypes.CDLL:
         "eig33_eigvals_host": ([P, S, P, P, P, I], I),
         "eig33_eigvalss_host": ([P, S, P, P, P, I], I),
         "eig33_multi_eigvals": ([P, S, P, P, P, I], I),
+        "eig33_multi_invariants": ([P, S, P, I], I),
+        "eig33_multi_eigvalss": ([P, S, P, P, P, I], I),
         "eig33cu_generate": ([I, U64, U64, S, P, P], I),
         "eig33cu_invariants_variant": ([P, S, I, P, P], I),
         "eig33cu_eigvals_naive": ([P, S, P, P, P], I),
@@ -373,3 +376,24 @@ def multi_eigvals(a, ngpu: int, *, return_invariants=False, return_flags=False) 
     _check(lib().eig33_multi_eigvals(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(ngpu)),
            "multi_eigvals")
     return EigResult(lam, inv, flags)
+
+
+def multi_eigvalss(a, ngpu: int, *, return_invariants=False, return_flags=False) -> EigResult:
+    """Host batch sharded over devices 0..ngpu-1 (eig33_multi_eigvalss);
+    ValueError if any matrix fails the symmetry gate."""
+    arr = _records_np(a)
+    n = arr.shape[0]
+    lam = np.empty((n, 3))
+    inv = np.empty((n, 4)) if return_invariants else None
+    flags = np.empty((n,), np.uint8) if return_flags else None
+    _check(lib().eig33_multi_eigvalss(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(ngpu)),
+           "multi_eigvalss")
+    return EigResult(lam, inv, flags)
+
+
+def multi_invariants(a, ngpu: int) -> np.ndarray:
+    """Host batch sharded over devices 0..ngpu-1 (eig33_multi_invariants): (n,4)."""
+    arr = _records_np(a)
+    inv = np.empty((arr.shape[0], 4))
+    _check(lib().eig33_multi_invariants(_ptr(arr), arr.shape[0], _ptr(inv), int(ngpu)), "multi_invariants")
+    return inv

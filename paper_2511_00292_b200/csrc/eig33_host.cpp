@@ -379,6 +379,41 @@ int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam,
   return EIG33_OK;
 }
 
+// Contiguous even-aligned shards, one host thread and device each;
+// no exchange between devices.  Pageable buffers go through each device's
+// staged pipeline (the host copy pool is shared); pinned ones are DMA'd directly.
+int run_multi(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
+              int ngpu, bool* any_notsym) {
+  int have = 0;
+  cudaError_t e = cudaGetDeviceCount(&have);
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDeviceCount", e);
+  if (ngpu < 1 || ngpu > have) return fail(EIG33_EINVAL, "ngpu out of range");
+  std::vector<int> rcs(ngpu, 0);
+  std::vector<char> anys(ngpu, 0);
+  std::vector<std::string> errs(ngpu);
+  std::vector<std::thread> th;
+  for (int g = 0; g < ngpu; ++g) {
+    const size_t lo = 2 * ((size_t)g * n / (2 * (size_t)ngpu));
+    const size_t hi = g + 1 == ngpu ? n : 2 * ((size_t)(g + 1) * n / (2 * (size_t)ngpu));
+    th.emplace_back([=, &rcs, &errs, &anys] {
+      bool any = false;
+      rcs[g] = run_device(op, h_a + lo * 9, hi - lo, h_inv ? h_inv + lo * 4 : nullptr,
+                          h_lam ? h_lam + lo * 3 : nullptr, h_flags ? h_flags + lo : nullptr, g,
+                          any_notsym ? &any : nullptr);
+      anys[g] = any;
+      if (rcs[g]) errs[g] = eig33cu_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int g = 0; g < ngpu; ++g)
+    if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
+  if (any_notsym) {
+    *any_notsym = false;
+    for (int g = 0; g < ngpu; ++g) *any_notsym = *any_notsym || anys[g];
+  }
+  return EIG33_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -419,33 +454,23 @@ int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_la
                         int ngpu) {
   eig33b::set_error("");
   if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_multi_eigvals: null pointer");
-  int have = 0;
-  cudaError_t e = cudaGetDeviceCount(&have);
-  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDeviceCount", e);
-  if (ngpu < 1 || ngpu > have) return fail(EIG33_EINVAL, "ngpu out of range");
-  // Page-lock the whole buffers once (portable: every device sees them pinned).
-  // Left to the per-device calls, shard boundaries that share a page would make
-  // all but the first registration fail and fall back to pageable copies.
-  const PinGuard pin_a(h_a, n * 9 * sizeof(double));
-  const PinGuard pin_l(h_lam, n * 3 * sizeof(double));
-  const PinGuard pin_i(h_inv, h_inv ? n * 4 * sizeof(double) : 0);
-  const PinGuard pin_f(h_flags, h_flags ? n : 0);
-  std::vector<int> rcs(ngpu, 0);
-  std::vector<std::string> errs(ngpu);
-  std::vector<std::thread> th;
-  for (int g = 0; g < ngpu; ++g) {
-    const size_t lo = 2 * ((size_t)g * n / (2 * (size_t)ngpu));
-    const size_t hi = g + 1 == ngpu ? n : 2 * ((size_t)(g + 1) * n / (2 * (size_t)ngpu));
-    th.emplace_back([=, &rcs, &errs] {
-      rcs[g] = run_device(Op::Eig, h_a + lo * 9, hi - lo, h_inv ? h_inv + lo * 4 : nullptr,
-                          h_lam + lo * 3, h_flags ? h_flags + lo : nullptr, g, nullptr);
-      if (rcs[g]) errs[g] = eig33cu_last_error();
-    });
-  }
-  for (auto& t : th) t.join();
-  for (int g = 0; g < ngpu; ++g)
-    if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
-  return EIG33_OK;
+  return run_multi(Op::Eig, h_a, n, h_inv, h_lam, h_flags, ngpu, nullptr);
+}
+
+int eig33_multi_invariants(const double* h_a, size_t n, double* h_inv, int ngpu) {
+  eig33b::set_error("");
+  if (n && (!h_a || !h_inv)) return fail(EIG33_EINVAL, "eig33_multi_invariants: null pointer");
+  return run_multi(Op::Inv, h_a, n, h_inv, nullptr, nullptr, ngpu, nullptr);
+}
+
+int eig33_multi_eigvalss(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
+                         int ngpu) {
+  eig33b::set_error("");
+  if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_multi_eigvalss: null pointer");
+  bool any = false;
+  const int rc = run_multi(Op::Sym, h_a, n, h_inv, h_lam, h_flags, ngpu, &any);
+  if (rc) return rc;
+  return any ? fail(EIG33_ENOTSYM, "matrix is not symmetric to working accuracy") : EIG33_OK;
 }
 
 }  // extern "C"

@@ -278,6 +278,27 @@ def test_host_staged_path_all_outputs():
         eig.eigvalss(s_)
 
 
+def test_multi_gpu_entry_points_on_available_devices():
+    """eig33_multi_{eigvals,eigvalss,invariants} over every visible device give
+    the single-device bits; asking for more devices than exist is an error."""
+    ng = torch.cuda.device_count()
+    a = U.mixed_corpus((1 << 17) + 11, 61)
+    s_ = a.copy()
+    s_[:, [3, 6, 7]] = s_[:, [1, 2, 5]]
+    r1 = eig.eigvals(a, return_invariants=True, return_flags=True)
+    rm = eig.multi_eigvals(a, ng, return_invariants=True, return_flags=True)
+    assert U.bit_equal(rm.lam, r1.lam).all() and U.bit_equal(rm.inv, r1.inv).all()
+    assert (rm.flags == r1.flags).all()
+    assert U.bit_equal(eig.multi_invariants(a, ng), r1.inv).all()
+    assert U.bit_equal(eig.multi_eigvalss(s_, ng).lam, eig.eigvalss(s_).lam).all()
+    k = s_.shape[0] // 8 + 5  # a grid record (entries O(1)): now clearly asymmetric
+    s_[k, 1] += 1.0
+    with pytest.raises(ValueError):
+        eig.multi_eigvalss(s_, ng)
+    with pytest.raises(ValueError):
+        eig.multi_eigvals(a, ng + 1)
+
+
 def test_shard_invariance_bitwise():
     """Results are identical whatever the contiguous even-aligned sharding
     (the multi-GPU driver's partition), emulated on one device."""

@@ -57,3 +57,30 @@ def test_fuzz_scaled_symmetric(vals, k):
     a = np.array([vals[0], vals[1], vals[2], vals[1], vals[3], vals[4], vals[2], vals[4], vals[5]])
     with np.errstate(all="ignore"):
         _check([np.ldexp(a, k)])
+
+
+# the moderate tier's range edges [2^-100, 2^100): grid mantissas (exact ties and
+# cancellations, near-equal diagonals) at exponents straddling both ends, so records
+# land just inside and just outside the guard-free tiers
+edge_exp = st.one_of(st.integers(-104, -94), st.integers(94, 101), st.integers(-3, 3))
+edge_entry = st.one_of(st.just(0.0),
+                       st.tuples(st.integers(-64, 64), edge_exp).map(lambda t: float(np.ldexp(t[0] / 16, t[1]))),
+                       st.tuples(st.integers(0, 3), edge_exp).map(
+                           lambda t: float(np.ldexp(1.0 + t[0] * 2.0 ** -52, t[1]))))
+
+
+@settings(max_examples=300, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.lists(st.lists(edge_entry, min_size=9, max_size=9), min_size=1, max_size=16))
+def test_fuzz_moderate_range_edges(rows):
+    with np.errstate(all="ignore"):
+        _check(rows)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(edge_entry, min_size=3, max_size=3), st.lists(edge_entry, min_size=6, max_size=6))
+def test_fuzz_edge_near_scalar(diag, off):
+    """c*I-like diagonals (equal or 1-ulp apart) with tiny or huge off-diagonals."""
+    c = diag[0]
+    a = np.array([c, off[0], off[1], off[2], np.nextafter(c, np.inf), off[3], off[4], off[5], c])
+    with np.errstate(all="ignore"):
+        _check([a])

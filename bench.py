@@ -40,17 +40,18 @@ HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 def parse():
     p = argparse.ArgumentParser()
-    p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=400)
-    p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--gpus", type=int, default=1, help="GPUs (N>1: launch under torchrun, one rank each)")
+    p.add_argument("--steps", type=int, default=400, help="timed steps (one 2^28-record launch each)")
+    p.add_argument("--warmup", type=int, default=5, help="untimed warm-up steps")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"],
+                   help="reference: the compiled reference core on all host cores (rank 0 only)")
     p.add_argument("--n", type=int, default=N_PER_GPU_DEFAULT, help="records per GPU")
-    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-steps", type=int, default=5, help="host-buffer (PCIe) end-to-end steps")
     p.add_argument("--no-power-roof", action="store_true",
-                   help="skip the idle / stream / chaotic-FP64 power probes after the timed region")
-    p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=10.0)
+                   help="skip the idle / data-path / stream / chaotic-FP64 power probes after the timed region")
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end measurement")
+    p.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU baseline leg (N=1 only anyway)")
+    p.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     return p.parse_args()
 
 

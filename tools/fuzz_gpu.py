@@ -2,7 +2,7 @@
 random bit patterns, mixed corpora, moderate-range edges and generated configs
 through eig33cu_eigvals (invariants + flags) and eig33cu_eigvalss, each checked
 against the compiled reference with the test suite's own gates.
-  python tools/fuzz_gpu.py [batches=8] [log2_records=22]"""
+  python tools/fuzz_gpu.py [batches=8] [log2_records=22] [first_batch=0]"""
 import os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np  # noqa: E402
@@ -30,9 +30,10 @@ def bits_corpus(n, rng):
 def main():
     batches = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 22)
+    first = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     t0 = time.time()
     checked = 0
-    for b in range(batches):
+    for b in range(first, first + batches):
         rng = np.random.default_rng(1000 + b)
         corpora = {
             "bits": bits_corpus(n, rng),

@@ -1,19 +1,31 @@
 """Throughput benchmark of the batched eig33 hot path (BASELINE.json metric:
 3x3 fp64 eigvals/sec at 1/2/4/8 B200; % of HBM/FP64 roofline).
 
-A step = one pass of the fused invariants -> eigenvalues kernel over one batch
-of BASELINE config 3 (general nonsymmetric A = V diag(l) V^-1, V Gaussian with
-cond2(V) <= 1e3, l ~ U[-10,10]), 2^28 records per GPU (19.3 GB in, 6.4 GB out),
-lambda-only output.  Weak scaling: rank r processes records
-[r*2^28, (r+1)*2^28) of one global counter-based corpus, no collective on the
-data path (torch.distributed is used only for the barrier and the max-over-ranks
-timing reduction).
+Workload (BASELINE configs[2], config 3): 2^28 general nonsymmetric records
+A = (V diag(l)) V^-1, V Gaussian with cond2(V) <= 1e3, l ~ U[-10,10] -- 19.3 GB
+in, 6.4 GB lambda out -- STRONG-sharded over the N GPUs exactly as SURVEY 8(e)
+and the C++ host driver eig33_multi_eigvals cut a batch: rank r evaluates the
+contiguous even-aligned shard shard_bounds(2^28, N, r).  A step = one
+eig33cu_eigvals launch per rank over its shard; the step time is the max over
+ranks (CUDA events on each rank's launch stream, all-gathered); value = 2^28 x
+steps / that time.  No collective on the data path: torch.distributed carries
+only the barrier and the timing/checksum reductions.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints one JSON line on rank 0.  --impl reference times the reference's own
-CPU implementation (oracle/_ref: the unmodified reference core compiled from
-/root/reference/proj/src; else the oracle port) on this box's host cores.
+Prints one JSON line on rank 0.  Besides the contract keys the line carries
+  roofline        FP64 pipe and HBM for k_fused, both fractions, the binding one on top
+  sustained       >= 3 s of back-to-back launches (time-blocked like the
+                  reference's own perf loop, proj/src/bench.cpp:222-241), own clocks
+  per_config      configs 1-5 at their BASELINE sizes, lambda and lambda+inv+flags
+  e2e             the same batch through eig33_eigvals_host (pinned host buffers,
+                  copies inside the timed region), one process per GPU
+  multi_driver    the same batch through eig33_multi_eigvals from ONE process
+                  over N devices (the north_star's host driver)
+  cpu_baseline    the compiled reference core on this host (N=1 only)
+--impl reference evaluates the same 2^28 records (host regeneration of the
+counter-based corpus, bit-identical to the device generator: oracle/libcorpus.so)
+with the compiled reference core (oracle/_ref) on all host cores.
 """
 import argparse
 import ctypes
@@ -31,79 +43,63 @@ sys.path.insert(0, ROOT)
 
 METRIC = "3×3 fp64 eigvals/sec at 1/2/4/8 B200; % of HBM/FP64 roofline"
 UNIT = "matrices/s"
-N_PER_GPU_DEFAULT = 1 << 28
+N_TOTAL_DEFAULT = 1 << 28
 SEED = 0x2511_00292
 BYTES_PER_REC = 96          # 72 B in + 24 B lambda out
+BYTES_PER_REC_FULL = 129    # + 32 B invariants + 1 B flags
 FP64_OPS_PER_REC = 357      # frozen algorithmic FP64-pipe count
 HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+SPEC_FP64_INST_PER_S = 148 * 64 * 1.965e9  # 148 SMs x 64 FP64 lanes x max SM clock
+CONFIG_SIZES = {1: 1 << 20, 2: 1 << 22, 3: 1 << 22, 4: 1 << 22, 5: 1 << 22}
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libeig33_ref.so")
+CORPUS_SO = os.path.join(ROOT, "oracle", "libcorpus.so")
+PROBES_SO = os.path.join(ROOT, "tools", "probes", "libeig33_probes.so")
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1, help="GPUs (N>1: launch under torchrun, one rank each)")
-    p.add_argument("--steps", type=int, default=400, help="timed steps (one 2^28-record launch each)")
-    p.add_argument("--warmup", type=int, default=5, help="untimed warm-up steps")
+    p.add_argument("--steps", type=int, default=20, help="timed steps (one launch per rank each)")
+    p.add_argument("--warmup", type=int, default=5, help="untimed warm-up steps (>= 3)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"],
                    help="reference: the compiled reference core on all host cores (rank 0 only)")
-    p.add_argument("--n", type=int, default=N_PER_GPU_DEFAULT, help="records per GPU")
-    p.add_argument("--e2e-steps", type=int, default=5, help="host-buffer (PCIe) end-to-end steps")
-    p.add_argument("--no-power-roof", action="store_true",
-                   help="skip the idle / data-path / stream / chaotic-FP64 power probes after the timed region")
-    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end measurement")
+    p.add_argument("--records", type=int, default=N_TOTAL_DEFAULT, help="records in the whole job (sharded over ranks)")
+    p.add_argument("--e2e-steps", type=int, default=3, help="host-buffer (PCIe) end-to-end steps")
+    p.add_argument("--sustained-seconds", type=float, default=3.0, help="length of the sustained sub-run (0: skip)")
+    p.add_argument("--no-per-config", action="store_true", help="skip the configs 1-5 block")
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end measurements")
+    p.add_argument("--no-multi-driver", action="store_true", help="skip the single-process eig33_multi_eigvals leg")
     p.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU baseline leg (N=1 only anyway)")
+    p.add_argument("--power-model", action="store_true",
+                   help="also run the energy-model probes (idle / data path / stream / chaotic DFMA power)")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
+    p.add_argument("--dry-run", action="store_true",
+                   help="CPU-only harness check (gloo, no kernels): sharding, timing reduction, JSON line")
     return p.parse_args()
 
 
-# ---------------------------------------------------------------------------
-# host-side corpus for the reference arm (same recipe as eig33_gen.cu config 3)
-# ---------------------------------------------------------------------------
-def config3_numpy(n, seed):
-    import numpy as np
+def shard_of(n, world, rank):
+    from paper_2511_00292_b200.shard import shard_bounds
 
-    rng = np.random.default_rng(seed)
-    out = np.empty((n, 9))
-    filled = 0
-    while filled < n:
-        m = int((n - filled) * 1.3) + 16
-        v = rng.standard_normal((m, 3, 3))
-        s = np.linalg.svd(v, compute_uv=False)
-        v = v[s[:, 0] / s[:, 2] <= 1e3]
-        lam = rng.uniform(-10, 10, (v.shape[0], 3))
-        # (V*D)*inverse_adjugate(V), reference association (bench.cpp:69-75)
-        vd = v * lam[:, None, :]
-        cof = np.empty_like(v)
-        cof[:, 0, 0] = v[:, 1, 1] * v[:, 2, 2] - v[:, 1, 2] * v[:, 2, 1]
-        cof[:, 0, 1] = v[:, 1, 2] * v[:, 2, 0] - v[:, 1, 0] * v[:, 2, 2]
-        cof[:, 0, 2] = v[:, 1, 0] * v[:, 2, 1] - v[:, 1, 1] * v[:, 2, 0]
-        cof[:, 1, 0] = v[:, 0, 2] * v[:, 2, 1] - v[:, 0, 1] * v[:, 2, 2]
-        cof[:, 1, 1] = v[:, 0, 0] * v[:, 2, 2] - v[:, 0, 2] * v[:, 2, 0]
-        cof[:, 1, 2] = v[:, 0, 1] * v[:, 2, 0] - v[:, 0, 0] * v[:, 2, 1]
-        cof[:, 2, 0] = v[:, 0, 1] * v[:, 1, 2] - v[:, 0, 2] * v[:, 1, 1]
-        cof[:, 2, 1] = v[:, 0, 2] * v[:, 1, 0] - v[:, 0, 0] * v[:, 1, 2]
-        cof[:, 2, 2] = v[:, 0, 0] * v[:, 1, 1] - v[:, 0, 1] * v[:, 1, 0]
-        det = (v[:, 0, 0] * cof[:, 0, 0] + v[:, 0, 1] * cof[:, 0, 1]) + v[:, 0, 2] * cof[:, 0, 2]
-        vinv = np.transpose(cof, (0, 2, 1)) / det[:, None, None]
-        a = np.einsum("nij,njk->nik", vd, vinv)
-        take = min(a.shape[0], n - filled)
-        out[filled:filled + take] = a[:take].reshape(take, 9)
-        filled += take
-    return np.ascontiguousarray(out)
+    return shard_bounds(n, world, rank)
 
 
-def cpu_lib():
-    """(ctypes lib, kind): the compiled reference core if built, else the port."""
-    ref = os.path.join(ROOT, "oracle", "_ref", "libeig33_ref.so")
-    if os.path.exists(ref):
-        return ctypes.CDLL(ref), "reference"
-    port = os.path.join(ROOT, "oracle", "liboracle.so")
-    if not os.path.exists(port):
-        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
-    return ctypes.CDLL(port), "port"
+def config_block(n_total, world):
+    """The workload description both arms print (identical dicts)."""
+    return {
+        "workload": "BASELINE config 3 (configs[2]): general nonsymmetric A=(V diag(l))V^-1, V~N(0,1) "
+                    "with cond2(V)<=1e3, l~U[-10,10]; lambda-only output",
+        "records_total": n_total,
+        "records_per_gpu": [hi - lo for lo, hi in (shard_of(n_total, world, r) for r in range(world))],
+        "sharding": "strong: contiguous even-aligned shards [2*floor(g*n/(2N)), ...) (SURVEY 8e)",
+        "parallelism": f"dp{world} (contiguous shards, no collective)",
+        "seed": SEED,
+        "generator": "counter-based eig33_gen_core.h (device eig33cu_generate == host oracle/libcorpus.so, bitwise)",
+        "l2": "inputs larger than L2 (19.3 GB per step at 2^28 records)",
+    }
 
 
 def host_description():
-    """CPU model and C library of the host the CPU legs run on."""
     model = platform.processor() or ""
     try:
         with open("/proc/cpuinfo") as f:
@@ -113,29 +109,65 @@ def host_description():
                     break
     except OSError:
         pass
-    return {"cpu_model": model, "libc": " ".join(platform.libc_ver()),
-            "host_threads": os.cpu_count()}
+    return {"cpu_model": model, "libc": " ".join(platform.libc_ver()), "host_threads": os.cpu_count()}
 
 
-def cpu_latency_ns(L, kind, iterations=1_000_000):
-    """The reference's own single-matrix latency discipline (src/bench.cpp:245-289):
-    eigvals_checksum_loop on generate_case(D2, U1, 1e-14), 10 timed blocks after a
-    warm-up block; returns (mean ns/eval, fastest ns/eval) or None for the port."""
-    if kind != "reference":
-        return None
+# ---------------------------------------------------------------------------
+# reference side (oracle/: the compiled reference core and the host corpus)
+# ---------------------------------------------------------------------------
+def ref_lib():
+    """The compiled reference core; no fallback -- a missing build is an error."""
+    if not os.path.exists(REF_SO):
+        raise FileNotFoundError(f"{REF_SO} missing: build it with `make -C oracle ref` where "
+                                "/root/reference exists (it travels to the GPU box prebuilt)")
+    L = ctypes.CDLL(REF_SO)
+    P, S, I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    L.ref_eigvals.argtypes = [P, S, P, P, I]
+    L.ref_checksum_loop.restype = ctypes.c_uint64
+    L.ref_checksum_loop.argtypes = [P, ctypes.c_uint64]
+    return L
+
+
+def host_corpus(config, n, seed, first=0, threads=None):
+    """Records [first, first+n) of a BASELINE config, regenerated on the host
+    (bit-identical to eig33cu_generate)."""
     import numpy as np
 
-    port = os.path.join(ROOT, "oracle", "liboracle.so")
-    if not os.path.exists(port):
+    if not os.path.exists(CORPUS_SO):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
-    O = ctypes.CDLL(port)
-    O.orc_generate_case.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
-                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-    d = np.array([1e-14])
-    m = np.empty(9)
-    O.orc_generate_case(1, 1, 1e-3, d.ctypes.data, 1, m.ctypes.data)  # D2 / U1 / delta 1e-14
-    L.ref_checksum_loop.restype = ctypes.c_uint64
-    L.ref_checksum_loop.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+    C = ctypes.CDLL(CORPUS_SO)
+    C.corpus_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_size_t,
+                                  ctypes.c_void_p, ctypes.c_int]
+    a = np.empty((n, 9))
+    rc = C.corpus_generate(config, seed, first, n, a.ctypes.data, threads or os.cpu_count() or 1)
+    if rc:
+        raise RuntimeError("corpus_generate failed")
+    return a
+
+
+def checksum_u64(x):
+    """Wrapping 64-bit sum of the records' bit patterns (numpy or torch)."""
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            return int(x.view(torch.int64).sum().item()) & (2 ** 64 - 1)
+    except ImportError:
+        pass
+    import numpy as np
+
+    return int(x.view(np.uint64).sum(dtype=np.uint64))
+
+
+def cpu_latency_ns(L, iterations=1_000_000):
+    """The reference's own single-matrix latency discipline (src/bench.cpp:245-289):
+    eigvals_checksum_loop on generate_case(D2, U1, 1e-14), 10 timed blocks after
+    a warm-up block; returns (mean ns/eval, fastest ns/eval)."""
+    import numpy as np
+
+    from tests._util import perf_matrix
+
+    m = np.ascontiguousarray(perf_matrix())
     reps, per = 10, iterations // 10
     L.ref_checksum_loop(m.ctypes.data, per // 10 + 1)
     ts = []
@@ -146,23 +178,18 @@ def cpu_latency_ns(L, kind, iterations=1_000_000):
     return statistics.mean(ts), min(ts)
 
 
-def cpu_eigvals_rate(a, seconds, threads):
-    """Stream eigvals over the host sample `a` repeatedly for ~`seconds` (>= 5
-    passes after one warm-up pass); returns (median-pass matrices/s, passes, kind)."""
+def cpu_eigvals_rate(L, a, seconds, threads):
+    """Stream eig33::eigvals over the host sample `a` for ~`seconds` (>= 5 passes
+    after a warm-up pass); returns (median-pass matrices/s, pass stats)."""
     import numpy as np
 
-    L, kind = cpu_lib()
     n = a.shape[0]
     lam = np.empty((n, 3))
-    pa, pl = a.ctypes.data_as(ctypes.c_void_p), lam.ctypes.data_as(ctypes.c_void_p)
 
     def one():
-        if kind == "reference":
-            L.ref_eigvals(pa, ctypes.c_size_t(n), pl, None, threads)
-        else:
-            L.orc_eigvals_mt(pa, ctypes.c_size_t(n), None, pl, threads)
+        L.ref_eigvals(a.ctypes.data, n, lam.ctypes.data, None, threads)
 
-    one()  # warm-up pass
+    one()
     t0 = time.perf_counter()
     ts = []
     while True:
@@ -171,35 +198,84 @@ def cpu_eigvals_rate(a, seconds, threads):
         ts.append(time.perf_counter() - t1)
         if time.perf_counter() - t0 >= seconds and len(ts) >= 5:
             break
-    # median pass (best/median of >= 5 passes); best in cpu_pass_stats
-    cpu_eigvals_rate.last = {"passes": len(ts), "median": n / statistics.median(ts),
-                             "best": n / min(ts), "mean": n * len(ts) / sum(ts)}
-    return n / statistics.median(ts), len(ts), kind
+    stats = {"passes": len(ts), "median": n / statistics.median(ts), "best": n / min(ts),
+             "mean": n * len(ts) / sum(ts)}
+    return n / statistics.median(ts), stats
+
+
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation (the compiled, unmodified core) on
+    every host core over the SAME 2^28 records the GPU arm evaluates; rank 0
+    only, the other ranks exit without work."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    n = args.records
+    L = ref_lib()
+    t0 = time.perf_counter()
+    a = host_corpus(3, n, SEED, 0, threads)
+    gen_s = time.perf_counter() - t0
+    lam = np.empty((n, 3))
+
+    def step():
+        L.ref_eigvals(a.ctypes.data, n, lam.ctypes.data, None, threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    v = n * args.steps / el
+    lat = cpu_latency_ns(L)
+    cfg = config_block(n, world)
+    cfg["input_checksum"] = f"{checksum_u64(a):016x}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"all {n} records of the GPU arm's batch (same seed, host regeneration "
+                                   f"bit-identical to the device corpus) per step; eig33::eigvals "
+                                   f"(oracle/_ref, the unmodified reference core) over contiguous shards "
+                                   f"on {threads} threads",
+                         "host_generation_s": gen_s,
+                         "latency_ns": {"mean": lat[0], "fastest": lat[1],
+                                        "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), "
+                                                "10 x 1e5 evals"},
+                         **host_description()},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (nvidia-smi during the timed regions)
 # ---------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampler (100 ms); stats cover only the samples taken between
-    mark_start() and mark_stop(), i.e. the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi sampler (100 ms) over the given GPUs; summaries cover the
+    samples taken inside a named window [mark(name, start), mark(name, stop)]."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, dev):
-        self.dev = dev
+    def __init__(self, devs):
+        self.devs = list(devs)
         self.proc = None
-        self.lines = []  # (host time, csv line)
-        self.t0 = self.t1 = None
+        self.lines = []
+        self.win = {}
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
-            self.th.start()
+                ["nvidia-smi", "-i", ",".join(map(str, self.devs)), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
             time.sleep(0.3)
         except OSError:
             self.proc = None
@@ -208,56 +284,166 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
-    def mark_start(self):
-        self.t0 = time.time()
+    def begin(self, name):
+        self.win[name] = [time.time(), None]
 
-    def mark_stop(self):
-        self.t1 = time.time()
-
-    def window(self, t0, t1):
-        """Median (board W, SM MHz) of the samples taken in [t0, t1]."""
-        pw, sm = [], []
-        for ts, ln in list(self.lines):
-            f = [x.strip() for x in ln.split(",")]
-            if t0 <= ts <= t1 and len(f) >= 3:
-                try:
-                    sm.append(float(f[0]))
-                    pw.append(float(f[2]))
-                except ValueError:
-                    pass
-        return (statistics.median(pw) if pw else None, statistics.median(sm) if sm else None)
+    def end(self, name):
+        self.win[name][1] = time.time()
 
     def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, name):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, pw, reasons = [], None, [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        t0 = self.t0 or 0.0
-        t1 = self.t1 or float("inf")
-        for ts, ln in self.lines:
+        t0, t1 = self.win[name]
+        sm, pw, mx, reasons = [], [], None, set()
+        for ts, ln in list(self.lines):
             if not (t0 <= ts <= t1 + 0.1):
                 continue
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
+            if len(f) < 8:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-                pw.append(float(f[2]))
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[3:7]):
+            for nm, v in zip(self.NAMES, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "power_w_median": statistics.median(pw) if pw else None,
-                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "gpus": self.devs,
+                "reasons": sorted(reasons)}
+
+    def power_window(self, t0, t1):
+        pw, sm = [], []
+        for ts, ln in list(self.lines):
+            f = [x.strip() for x in ln.split(",")]
+            if t0 <= ts <= t1 and len(f) >= 4:
+                try:
+                    sm.append(float(f[1]))
+                    pw.append(float(f[3]))
+                except ValueError:
+                    pass
+        return (statistics.median(pw) if pw else None, statistics.median(sm) if sm else None)
+
+
+# ---------------------------------------------------------------------------
+# measurement helpers (GPU arm)
+# ---------------------------------------------------------------------------
+def probes_lib():
+    """tools/probes/libeig33_probes.so: FP64 issue-rate and energy probes
+    (measurement only; never part of the product library)."""
+    if not os.path.exists(PROBES_SO):
+        from paper_2511_00292_b200 import build
+
+        build.build_probes()
+    L = ctypes.CDLL(PROBES_SO)
+    L.eig33_probe_fp64_rate.restype = ctypes.c_double
+    L.eig33_probe_fp64_rate.argtypes = [ctypes.c_int]
+    L.eig33_probe_fp64_chaos.restype = ctypes.c_double
+    L.eig33_probe_fp64_chaos.argtypes = [ctypes.c_double]
+    L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
+    L.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
+    return L
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic():
+    """Per-record DRAM bytes of k_fused from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k_fused.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("records_per_launch")
+    except (OSError, ValueError):
+        return None, None
+
+
+def roofline(rate_per_gpu, bytes_per_rec, hbm_peak, hbm_src, fp64_peak, fp64_src):
+    """Both roofs for one kernel at `rate_per_gpu` records/s; the binding roof
+    (the slower one for this record mix) on top."""
+    hbm_ach = rate_per_gpu * bytes_per_rec / 1e9
+    fp64_ach = rate_per_gpu * FP64_OPS_PER_REC / 1e12
+    hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
+           "peak_source": hbm_src, "bytes_per_record": bytes_per_rec}
+    fp64 = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "T fp64-inst/s",
+            "frac": fp64_ach / fp64_peak if fp64_peak else None, "peak_source": fp64_src,
+            "frac_of_spec": fp64_ach * 1e12 / SPEC_FP64_INST_PER_S,
+            "spec_peak": SPEC_FP64_INST_PER_S / 1e12,
+            "ops_per_record": FP64_OPS_PER_REC}
+    binding = fp64 if (fp64["frac"] or 0) >= hbm["frac"] else hbm
+    out = dict(binding)
+    out["both"] = {"hbm": hbm, "fp64": fp64}
+    return out
+
+
+def time_launches(fn, stream, reps, torch):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def per_config_block(L, eig, torch, dev, stream, hbm_peak, hbm_src, fp64_peak, fp64_src, reps=20):
+    """Configs 1-5 at their BASELINE sizes (config 3 at 2^22 here; its 2^28 is
+    the headline): lambda only (96 B/record) and lambda + invariants + flags
+    (129 B/record, what configs 1, 4 and 5 ask for).  Burst rates: 20
+    launches each after 3 warm-ups, on a GPU that idled 0.5 s first."""
+    out = {}
+    for cfg, n in CONFIG_SIZES.items():
+        with torch.cuda.stream(stream):
+            a = eig.generate(cfg, n, seed=SEED + cfg, device=dev)
+            lam = torch.empty((n, 3), dtype=torch.float64, device=dev)
+            inv = torch.empty((n, 4), dtype=torch.float64, device=dev)
+            fl = torch.empty((n,), dtype=torch.uint8, device=dev)
+        stream.synchronize()
+        pa, pl, pi, pf = (ctypes.c_void_p(x.data_ptr()) for x in (a, lam, inv, fl))
+        st = ctypes.c_void_p(stream.cuda_stream)
+        row = {"records": n}
+        for mode, args_, bpr in (("lam", (None, pl, None), BYTES_PER_REC),
+                                 ("lam_inv_flags", (pi, pl, pf), BYTES_PER_REC_FULL)):
+            def fn(args_=args_):
+                rc = L.eig33cu_eigvals(pa, n, *args_, st)
+                if rc:
+                    raise RuntimeError(L.eig33cu_last_error().decode())
+            time.sleep(0.5)
+            for _ in range(3):
+                fn()
+            ms = time_launches(fn, stream, reps, torch)
+            rate = n / (ms * 1e-3)
+            rf = roofline(rate, bpr, hbm_peak, hbm_src, fp64_peak, fp64_src)
+            row[mode] = {"value": rate, "unit": UNIT, "ms_per_launch": ms, "launches": reps,
+                         "kernels_per_launch": 2 if mode == "lam_inv_flags" else 1,
+                         "roofline": {"bound": rf["bound"], "frac": rf["frac"],
+                                      "frac_hbm": rf["both"]["hbm"]["frac"],
+                                      "frac_fp64": rf["both"]["fp64"]["frac"],
+                                      "bytes_per_record": bpr}}
+        if cfg == 4 or cfg == 5:
+            adv = int((fl.to(torch.int32) & 1).sum().item())
+            row["advisory_share"] = adv / n
+        out[str(cfg)] = row
+        del a, lam, inv, fl
+    return out
 
 
 def pcie_rates(torch, h_a, h_l, dev):
@@ -291,39 +477,18 @@ def pcie_rates(torch, h_a, h_l, dev):
     return r
 
 
-def power_limit_w(dev):
-    try:
-        out = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=power.limit",
-                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                             timeout=20).stdout.strip()
-        return float(out.splitlines()[0])
-    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
-        return 1000.0
-
-
-def power_roof(L, clocks, pa, pl, n, st, stream, dev):
-    """Energy roof at the board power limit: measure, on this
-    GPU and this run's data, the idle draw, the energy per record of the
-    kernel's own data path with the arithmetic removed (eig33_probe_memonly:
-    TMA ring, tier tests, lambda stores), of a plain 72 B-in / 24 B-out stream
-    (eig33_probe_stream, for reference), and the energy per FP64 instruction
-    on chaotic operands (eig33_probe_fp64_chaos);
-    roof = (limit - idle) / (E_datapath + ops_per_record * E_fp64)."""
-    import torch
-
-    if not clocks.proc:
-        return None
-    L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
-                                     ctypes.c_void_p]
-    L.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
-    L.eig33_probe_fp64_chaos.restype = ctypes.c_double
-    L.eig33_probe_fp64_chaos.argtypes = [ctypes.c_double]
+def power_model(P, clocks, pa, pl, n, st, stream, dev, torch):
+    """Optional energy MODEL (--power-model).  It divides
+    the board power limit by energy per record built from this kernel's own
+    data path with the arithmetic removed (eig33_probe_memonly) plus 357 x the
+    energy of a chaotic-operand DFMA -- a model partly defined by the kernel
+    itself, reported as supporting evidence only, never as the roofline."""
     torch.cuda.synchronize()
     t = time.time()
     time.sleep(2.0)
-    p_idle, _ = clocks.window(t + 1.0, time.time())
+    p_idle, _ = clocks.power_window(t + 1.0, time.time())
+
     def probe(fn, secs=2.5):
-        """~secs of back-to-back launches: (records/s by CUDA events, median W, MHz)."""
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         fn()
@@ -337,313 +502,330 @@ def power_roof(L, clocks, pa, pl, n, st, stream, dev):
                 stream.synchronize()
         e1.record(stream)
         e1.synchronize()
-        w, mhz = clocks.window(t + 1.0, time.time())
+        w, mhz = clocks.power_window(t + 1.0, time.time())
         return k * n / (e0.elapsed_time(e1) * 1e-3), w, mhz
 
-    rec_s, p_stream, mhz_stream = probe(lambda: L.eig33_probe_stream(pa, n, pl, st))
-    time.sleep(1.0)
-    dp_s, p_dp, mhz_dp = probe(lambda: L.eig33_probe_memonly(pa, n, pl, st))
+    dp_s, p_dp, mhz_dp = probe(lambda: P.eig33_probe_memonly(pa, n, pl, st))
     time.sleep(1.0)
     t = time.time()
-    op_s = L.eig33_probe_fp64_chaos(2.5)
-    p_fp64, mhz_fp64 = clocks.window(t + 1.0, time.time())
-    if None in (p_idle, p_stream, p_dp, p_fp64) or op_s <= 0:
+    op_s = P.eig33_probe_fp64_chaos(2.5)
+    p_fp64, mhz_fp64 = clocks.power_window(t + 1.0, time.time())
+    if None in (p_idle, p_dp, p_fp64) or op_s <= 0:
         return None
-    cap = power_limit_w(dev)
-    e_rec = (p_stream - p_idle) / rec_s
+    cap = 1000.0
     e_dp = (p_dp - p_idle) / dp_s
     e_op = (p_fp64 - p_idle) / op_s
     e_total = e_dp + FP64_OPS_PER_REC * e_op
-    return {"idle_w": p_idle, "limit_w": cap,
-            "datapath": {"records_per_s": dp_s, "w": p_dp, "sm_mhz": mhz_dp, "nj_per_record": e_dp * 1e9,
-                         "probe": "eig33_probe_memonly: k_fused's TMA ring, tier tests and stores, "
-                                  "no arithmetic"},
-            "stream": {"records_per_s": rec_s, "w": p_stream, "sm_mhz": mhz_stream,
-                       "nj_per_record": e_rec * 1e9},
-            "fp64_chaos": {"inst_per_s": op_s, "w": p_fp64, "sm_mhz": mhz_fp64,
-                           "pj_per_inst": e_op * 1e12},
+    return {"kind": "model (self-referential: data-path term measured on this kernel with its "
+                    "arithmetic removed); supporting evidence, not a roofline",
+            "idle_w": p_idle, "limit_w": cap,
+            "datapath": {"records_per_s": dp_s, "w": p_dp, "sm_mhz": mhz_dp, "nj_per_record": e_dp * 1e9},
+            "fp64_chaos": {"inst_per_s": op_s, "w": p_fp64, "sm_mhz": mhz_fp64, "pj_per_inst": e_op * 1e12},
             "nj_per_record_model": e_total * 1e9,
-            "roof_records_per_s": (cap - p_idle) / e_total}
-
-
-def measured_peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
-    except (OSError, ValueError):
-        return {}
-
-
-def ncu_traffic():
-    """Per-launch DRAM bytes of k_fused from the committed ncu --set full summary."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_k_fused.json")) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("records_per_launch")
-    except (OSError, ValueError):
-        return None, None
+            "model_records_per_s": (cap - p_idle) / e_total}
 
 
 # ---------------------------------------------------------------------------
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    import numpy as np
-
-    threads = os.cpu_count() or 1
-    sample = 1 << 22
-    a = config3_numpy(sample, SEED)
-    L, kind = cpu_lib()
-    lam = np.empty((sample, 3))
-    pa, pl = a.ctypes.data_as(ctypes.c_void_p), lam.ctypes.data_as(ctypes.c_void_p)
-
-    def step():
-        if kind == "reference":
-            L.ref_eigvals(pa, ctypes.c_size_t(sample), pl, None, threads)
-        else:
-            L.orc_eigvals_mt(pa, ctypes.c_size_t(sample), None, pl, threads)
-
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    el = time.perf_counter() - t0
-    v = sample * args.steps / el
-    lat = cpu_latency_ns(L, kind)
-    if lat is not None:
-        lat = {"mean": lat[0], "fastest": lat[1],
-               "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), 10 x 1e5 evals"}
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "config3 general nonsymmetric, cond2(V)<=1e3, lambda~U[-10,10]",
-                   "records_per_step": sample, "outputs": "lambda only"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{sample} config-3 records per step (numpy-generated, seed {SEED}), "
-                                   f"eig33::eigvals streamed over contiguous shards on {threads} threads",
-                         "latency_ns": lat, **host_description()},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
 
     import paper_2511_00292_b200 as eig
-    from paper_2511_00292_b200.shard import weak_range
 
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist = None
+    dist = hostpg = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
 
         dist.init_process_group("nccl", device_id=dev)
+        # Host-side synchronisation goes through a gloo group: an NCCL barrier
+        # would leave a spinning kernel on the waiting ranks' GPUs while rank 0
+        # drives all devices in the multi-driver leg.
+        hostpg = dist.new_group(backend="gloo")
 
     def barrier():
         if dist is not None:
-            dist.barrier()
+            dist.barrier(group=hostpg)
+
+    def gather(x):
+        if dist is None:
+            return [float(x)]
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=hostpg)
+        return [float(o.item()) for o in out]
+
+    def gather_int(x):
+        if dist is None:
+            return [x]
+        out = [None] * world
+        dist.all_gather_object(out, x, group=hostpg)
+        return out
 
     L = eig.lib()
-    n = args.n
+    P = probes_lib()
+    n_total = args.records
+    lo, hi = shard_of(n_total, world, rank)
+    n = hi - lo
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
-        lo, _ = weak_range(n, rank)  # this rank's slice of the global corpus
         a = eig.generate(3, n, seed=SEED, first_index=lo, device=dev)
         lam = torch.empty((n, 3), dtype=torch.float64, device=dev)
     stream.synchronize()
     pa, pl = ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(lam.data_ptr())
     st = ctypes.c_void_p(stream.cuda_stream)
+    # checksum of the whole job's records (wrapping 64-bit sum over ranks)
+    input_checksum = sum(int(c) for c in gather_int(checksum_u64(a))) & (2 ** 64 - 1)
 
     def step():
         rc = L.eig33cu_eigvals(pa, n, None, pl, None, st)
         if rc:
             raise RuntimeError(L.eig33cu_last_error().decode())
 
-    # FP64 issue-rate peak on this GPU (roofline denominator), before the run
-    L.eig33_probe_fp64_rate.restype = ctypes.c_double
-    L.eig33_probe_fp64_rate.argtypes = [ctypes.c_int]
-    fp64_rate = L.eig33_probe_fp64_rate(20)
+    # FP64 issue-rate peaks on this GPU (roofline denominators): burst (for the
+    # short headline region) and sustained chaotic-operand DFMA (for the long run)
+    fp64_burst = P.eig33_probe_fp64_rate(20)
+    devs = list(range(world)) if rank == 0 else [local_rank]
+    clocks = Clocks(devs if rank == 0 else [local_rank])
+    clocks.start()
 
     for _ in range(args.warmup):
         step()
     stream.synchronize()
-    barrier()
-    clocks = Clocks(local_rank)
-    clocks.start()
     torch.cuda.synchronize()
     barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    clocks.mark_start()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    e1.synchronize()
-    clocks.mark_stop()
+    clocks.begin("headline")
+    ms_rank = time_launches(step, stream, args.steps, torch) * args.steps
+    clocks.end("headline")
     torch.cuda.synchronize()
     barrier()
-    proof = None if args.no_power_roof else power_roof(L, clocks, pa, pl, n, st, stream, dev)
-    clk = clocks.stop()
-    if proof is not None:  # the stream probe wrote over lam: restore the step's result
-        step()
-        stream.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    per_rank_ms = gather(ms_rank)
+    ms_max = max(per_rank_ms)
     ms_step = ms_max / args.steps
-    total = n * world
-    value = total * args.steps / (ms_max * 1e-3)
+    value = n_total * args.steps / (ms_max * 1e-3)
 
-    # ---- e2e through the public host-buffer API (pinned host in/out) ----
+    # ---- sustained sub-run: time-blocked, >= args.sustained_seconds ----
+    sustained = None
+    if args.sustained_seconds > 0:
+        time.sleep(0.5)
+        barrier()
+        clocks.begin("sustained")
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.time()
+        k = 0
+        while time.time() - t0 < args.sustained_seconds:
+            for _ in range(8):
+                step()
+            k += 8
+            stream.synchronize()
+        e1.record(stream)
+        e1.synchronize()
+        clocks.end("sustained")
+        ks = gather(k)
+        mss = gather(e0.elapsed_time(e1))
+        # each rank ran its own launch count; the job's step time is the slowest
+        # rank's mean launch time
+        ms_sus = max(m / kk for m, kk in zip(mss, ks))
+        sustained = {"value": n_total / (ms_sus * 1e-3), "unit": UNIT, "seconds": max(mss) / 1e3,
+                     "launches_per_rank": ks, "ms_per_step": ms_sus}
+        barrier()
+    fp64_sus = P.eig33_probe_fp64_chaos(2.5) if args.sustained_seconds > 0 else 0.0
+
+    # ---- e2e: the same shard through the public host-buffer API, pinned ----
     e2e = None
+    h_a = h_l = None
     if not args.no_e2e:
-        # Same workload through the host-buffer API; if the box cannot pin
-        # 96 B/record for every local rank, time a prefix and say so.
-        ne = n
-        try:
-            import psutil
-
-            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-            budget = psutil.virtual_memory().available * 0.4 / max(1, local_world)
-            ne = min(n, int(budget // 96) & ~1)
-        except ImportError:
-            pass
-        h_a = torch.empty((ne, 9), dtype=torch.float64, pin_memory=True)
-        h_a.copy_(a[:ne])
-        h_l = torch.empty((ne, 3), dtype=torch.float64, pin_memory=True)
+        h_a = torch.empty((n, 9), dtype=torch.float64, pin_memory=True)
+        h_a.copy_(a)
+        h_l = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
         pha, phl = ctypes.c_void_p(h_a.data_ptr()), ctypes.c_void_p(h_l.data_ptr())
-        rc = L.eig33_eigvals_host(pha, ne, None, phl, None, local_rank)  # warm (staging alloc)
+        rc = L.eig33_eigvals_host(pha, n, None, phl, None, local_rank)  # warm (staging alloc)
         if rc:
             raise RuntimeError(L.eig33cu_last_error().decode())
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            rc = L.eig33_eigvals_host(pha, ne, None, phl, None, local_rank)
+            rc = L.eig33_eigvals_host(pha, n, None, phl, None, local_rank)
             if rc:
                 raise RuntimeError(L.eig33cu_last_error().decode())
         el = time.perf_counter() - t0
-        te = torch.tensor([el], dtype=torch.float64, device=dev)
-        if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        el = float(te.item())
-        same = bool(torch.equal(h_l.view(torch.int64), lam[:ne].cpu().view(torch.int64)))
-        # PCIe roof for this path, measured on this box with the same pinned
-        # buffers: H2D alone, D2H alone, and both at once on two streams (the
-        # link is not fully duplex here: concurrent D2H slows H2D).
+        el_max = max(gather(el))
+        same = bool(torch.equal(h_l.view(torch.int64), lam.cpu().view(torch.int64)))
+        same_all = min(gather(1.0 if same else 0.0)) == 1.0
         link = pcie_rates(torch, h_a, h_l, dev)
-        # duplex model: each record's 24 B of D2H runs alongside H2D at the
-        # concurrent rates, the rest of its 72 B of H2D at the solo rate.
         t_rec = 24 / link["d2h_concurrent_gbs"] + \
             max(0.0, 72 - link["h2d_concurrent_gbs"] * 24 / link["d2h_concurrent_gbs"]) / link["h2d_gbs"]
         model = 1e9 / t_rec
-        e2e_value = ne * world * args.e2e_steps / el
-        e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * 72,
-               "d2h_bytes_per_step": ne * 24, "steps": args.e2e_steps, "records_per_gpu_per_step": ne,
-               "api": "eig33_eigvals_host (pinned host buffers, chunked H2D/kernel/D2H over 3 streams)",
-               "bitwise_equal_to_device_path": same,
+        e2e_value = n_total * args.e2e_steps / el_max
+        e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_total * 72,
+               "d2h_bytes_per_step": n_total * 24, "steps": args.e2e_steps,
+               "api": "eig33_eigvals_host per rank on its shard (pinned host buffers, chunked "
+                      "H2D/kernel/D2H over 3 streams); wall clock, max over ranks",
+               "bitwise_equal_to_device_path": same_all,
                "pcie_roofline": {"bound": "pcie", "h2d_gbs_measured": link["h2d_gbs"],
                                  "d2h_gbs_measured": link["d2h_gbs"],
                                  "concurrent_h2d_gbs": link["h2d_concurrent_gbs"],
                                  "concurrent_d2h_gbs": link["d2h_concurrent_gbs"],
-                                 "achieved_h2d_gbs": e2e_value / world * 72 / 1e9,
-                                 "h2d_only_roof_records_per_s": link["h2d_gbs"] * 1e9 / 72,
-                                 "duplex_model_records_per_s": model,
+                                 "duplex_model_records_per_s_per_gpu": model,
                                  "frac": e2e_value / world / model}}
-        del h_a, h_l
+        if world > 1:
+            del h_a, h_l
+            h_a = h_l = None
+    barrier()
 
+    # ---- power model (optional) ----
+    pmodel = None
+    if args.power_model and rank == 0:
+        pmodel = power_model(P, clocks, pa, pl, n, st, stream, dev, torch)
+        step()
+        stream.synchronize()
+    barrier()
+
+    # ---- per-config block (rank 0; the others wait) ----
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs") or HBM_PEAK_FALLBACK
+    hbm_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "of fallback"
+    fp64_src_b = ("of builder-measured: burst DFMA issue rate on this GPU (tools/probes "
+                  "eig33_probe_fp64_rate, 20 x 11 ms)")
+    fp64_src_s = ("of builder-measured: sustained chaotic-operand DFMA rate on this GPU, 2.5 s "
+                  "(tools/probes eig33_probe_fp64_chaos)")
+    per_config = None
+    if not args.no_per_config and rank == 0:
+        per_config = per_config_block(L, eig, torch, dev, stream, hbm_peak, hbm_src,
+                                      fp64_burst / 1e12, fp64_src_b)
+    barrier()
+
+    # ---- multi-driver: one process, eig33_multi_eigvals over N devices ----
+    multi = None
+    if not args.no_e2e and not args.no_multi_driver:
+        del a, lam
+        torch.cuda.empty_cache()
+        barrier()
+        if rank == 0:
+            if h_a is None:  # N>1: the whole batch on rank 0's host, pinned
+                h_a = torch.empty((n_total, 9), dtype=torch.float64, pin_memory=True)
+                h_l = torch.empty((n_total, 3), dtype=torch.float64, pin_memory=True)
+                sl = 1 << 25
+                for s0 in range(0, n_total, sl):
+                    m = min(sl, n_total - s0)
+                    h_a[s0:s0 + m].copy_(eig.generate(3, m, seed=SEED, first_index=s0, device=dev))
+                torch.cuda.empty_cache()
+            pha, phl = ctypes.c_void_p(h_a.data_ptr()), ctypes.c_void_p(h_l.data_ptr())
+            rc = L.eig33_multi_eigvals(pha, n_total, None, phl, None, world)  # warm
+            if rc:
+                raise RuntimeError(L.eig33cu_last_error().decode())
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                rc = L.eig33_multi_eigvals(pha, n_total, None, phl, None, world)
+                if rc:
+                    raise RuntimeError(L.eig33cu_last_error().decode())
+            el = time.perf_counter() - t0
+            multi = {"value": n_total * args.e2e_steps / el, "unit": UNIT, "ngpu": world,
+                     "steps": args.e2e_steps, "h2d_bytes_per_step": n_total * 72,
+                     "d2h_bytes_per_step": n_total * 24,
+                     "api": "eig33_multi_eigvals (one process, one host thread + stream set per device, "
+                            "pinned host buffers); wall clock"}
+        barrier()
+    h_a = h_l = None
+
+    clocks.stop()
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    # ---- roofline ----
-    peaks = measured_peaks()
-    hbm_peak = peaks.get("hbm_gbs") or HBM_PEAK_FALLBACK
-    per_launch_s = ms_step * 1e-3
-    hbm_ach = n * BYTES_PER_REC / per_launch_s / 1e9
-    fp64_ach = n * FP64_OPS_PER_REC / per_launch_s / 1e12
-    # The timed region is a long step (~3 s), so the denominator is the sustained
-    # FP64 rate: chaotic-operand DFMA over 2.5 s from the energy-roof probes (it
-    # never reaches the power cap); the 11 ms burst probe if those were skipped.
-    sustained = proof["fp64_chaos"]["inst_per_s"] if proof else 0.0
-    fp64_peak = (sustained if sustained > 0 else fp64_rate) / 1e12 if max(sustained, fp64_rate) > 0 else None
-    fp64_src = ("measured on this GPU: sustained DFMA rate, chaotic operands, 2.5 s "
-                "(eig33_probe_fp64_chaos)" if sustained > 0 else
-                "measured on this GPU: burst DFMA issue rate (eig33_probe_fp64_rate)")
+    per_gpu = value / world
+    rf = roofline(per_gpu, BYTES_PER_REC, hbm_peak, hbm_src, fp64_burst / 1e12, fp64_src_b)
     traffic, recs = ncu_traffic()
-    traffic_per_launch = traffic * n / recs if traffic and recs else None
-    hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
-           "frac": hbm_ach / hbm_peak,
-           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks.get("hbm_gbs") else "fallback"}
-    fp64 = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "T fp64-inst/s",
-            "frac": fp64_ach / fp64_peak if fp64_peak else None,
-            "peak_source": fp64_src, "burst_peak": fp64_rate / 1e12,
-            "ops_per_record": FP64_OPS_PER_REC}
-    # the binding roof is the slower one (BASELINE north_star): the one with the higher frac
-    binding = fp64 if (fp64["frac"] or 0) >= hbm["frac"] else hbm
-    roofline = dict(binding)
-    roofline["traffic"] = traffic_per_launch
-    roofline["algorithmic_bytes_per_launch"] = n * BYTES_PER_REC
-    roofline["kernel"] = "k_fused<eigvals,TMA> (1 launch per step)"
-    roofline["both"] = {"hbm": hbm, "fp64": fp64}
-    # The 1000 W board limit binds before either roof (DESIGN.md, "Power"):
-    # report the energy per record the clocks record implies.
-    if clk.get("power_w_median"):
-        roofline["power"] = {"w_median": clk["power_w_median"], "cap_w": 1000.0,
-                             "nj_per_record": clk["power_w_median"] / (value / world) * 1e9,
-                             "sm_mhz_median": clk.get("sm_mhz")}
-        if proof:
-            roofline["power"]["cap_w"] = proof["limit_w"]
-            roofline["power"]["energy_roof"] = proof
-            roofline["power"]["frac"] = (value / world) / proof["roof_records_per_s"]
+    rf["traffic"] = traffic * n / recs if traffic and recs else None
+    rf["traffic_source"] = "profiles/ncu_k_fused.json (ncu --set full, dram__bytes_read+write per record x records per launch)"
+    rf["algorithmic_bytes_per_launch"] = n * BYTES_PER_REC
+    rf["kernel"] = "k_fused<eigvals,TMA> (1 launch per step per rank)"
+    if sustained:
+        sustained["clocks"] = clocks.summary("sustained")
+        sustained["roofline"] = roofline(sustained["value"] / world, BYTES_PER_REC, hbm_peak, hbm_src,
+                                         fp64_sus / 1e12 if fp64_sus > 0 else None, fp64_src_s)
+    if pmodel:
+        rf["power_model"] = pmodel
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
-        samp = 1 << 22
-        a_host = a[:samp].cpu().numpy()
+        Lr = ref_lib()
         threads = os.cpu_count() or 1
-        rate, passes, kind = cpu_eigvals_rate(a_host, args.cpu_seconds, threads)
-        stats = dict(cpu_eigvals_rate.last)
-        rate1, passes1, _ = cpu_eigvals_rate(a_host[: 1 << 20], min(args.cpu_seconds, 3.0), 1)
-        lat = cpu_latency_ns(*cpu_lib())
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"first {samp} records of this run's config-3 batch, median of {passes} timed "
-                         f"passes (~{args.cpu_seconds:.0f} s), eig33::eigvals on {threads} threads "
-                         f"(contiguous shards, one thread pinned per core)",
+        samp = min(1 << 22, n_total)
+        a_host = host_corpus(3, samp, SEED, 0, threads)
+        rate, stats = cpu_eigvals_rate(Lr, a_host, args.cpu_seconds, threads)
+        rate1, stats1 = cpu_eigvals_rate(Lr, a_host[: 1 << 20], min(args.cpu_seconds, 3.0), 1)
+        lat = cpu_latency_ns(Lr)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+               "sample": f"first {samp} records of this run's config-3 batch (host regeneration, bitwise the "
+                         f"same records), median of {stats['passes']} passes (~{args.cpu_seconds:.0f} s), "
+                         f"eig33::eigvals (oracle/_ref) on {threads} threads",
                "passes": stats,
-               "one_core": {"value": rate1, "unit": UNIT,
-                            "sample": f"first {1 << 20} records, {passes1} passes on 1 thread"},
-               "latency_ns": None if lat is None else
-               {"mean": lat[0], "fastest": lat[1],
-                "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), 10 x 1e5 evals"},
+               "one_core": {"value": rate1, "unit": UNIT, "sample": f"first {1 << 20} records, "
+                                                                  f"{stats1['passes']} passes on 1 thread"},
+               "latency_ns": {"mean": lat[0], "fastest": lat[1],
+                              "loop": "eigvals_checksum_loop on generate_case(D2,U1,1e-14), 10 x 1e5 evals"},
                **host_description()}
 
+    cfg = config_block(n_total, world)
+    cfg["input_checksum"] = f"{input_checksum:016x}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "BASELINE config 3 (configs[2]): general nonsymmetric A=(V diag(l))V^-1, "
-                               "V~N(0,1) with cond2(V)<=1e3, l~U[-10,10]; lambda-only output",
-                   "records_per_gpu": n, "parallelism": f"dp{world} (contiguous shards, no collective)",
-                   "seed": SEED, "l2": "inputs larger than L2 (19.3 GB per GPU per step)"},
-        "roofline": roofline,
+        "config": cfg,
+        "per_rank_ms": per_rank_ms,
+        "roofline": rf,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "multi_driver": multi,
         "gpu_launches": args.steps,
-        "clocks": clk,
-        "fp64_probe_inst_per_s": fp64_rate,
+        "clocks": clocks.summary("headline"),
+        "sustained": sustained,
+        "per_config": per_config,
+        "fp64_probe_inst_per_s": {"burst": fp64_burst, "sustained": fp64_sus,
+                                  "spec_at_max_clock": SPEC_FP64_INST_PER_S},
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_dry(args, rank, world):
+    """CPU-only check of the N-rank harness (gloo): the shard each rank owns,
+    the max-over-ranks timing reduction and the JSON line's shape.  No kernel
+    runs; the 'step' is a fixed host sleep per record so rank times differ."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, hi = shard_of(args.records, world, rank)
+    t0 = time.perf_counter()
+    for _ in range(args.warmup + args.steps):
+        time.sleep((hi - lo) * 1e-9)
+    ms = (time.perf_counter() - t0) * 1e3 * args.steps / (args.warmup + args.steps)
+    t = torch.tensor([ms, float(lo), float(hi)], dtype=torch.float64)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(out, t)
+    else:
+        out = [t]
+    if rank == 0:
+        per = [float(o[0]) for o in out]
+        shards = [[int(o[1]), int(o[2])] for o in out]
+        print(json.dumps({"impl": "dry-run", "metric": METRIC, "value": args.records * args.steps / (max(per) * 1e-3),
+                          "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": max(per) / args.steps, "higher_is_better": True, "scaling": "strong",
+                          "per_rank_ms": per, "shards": shards, "config": config_block(args.records, world)}),
+              flush=True)
+    if world > 1:
         dist.destroy_process_group()
 
 
@@ -652,7 +834,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, world, local_rank)

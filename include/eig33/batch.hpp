@@ -9,7 +9,8 @@
 //       batches  InvariantSet invariants(const Mat3&, AlgorithmVariant)  invariants.hpp:74
 //   eig33::eigvals(const Mat3*, n, EigenTriple*)
 //       batches  EigenTriple eigvals(const Mat3&)                        eigensolver.hpp:39
-//   eig33::eigvalss(const Mat3*, n, EigenTriple*)   throws NotSymmetric like the scalar call
+//   eig33::eigvalss(const Mat3*, n, EigenTriple*)   throws NotSymmetricAt (a NotSymmetric
+//                                                   carrying the first bad index)
 //       batches  EigenTriple eigvalss(const Mat3&)                       eigensolver.hpp:45
 //   eig33::eigvals_packed(const Mat3*, n, double* lam, double* inv)   packed 24 B / 32 B outputs
 //
@@ -62,11 +63,23 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// What the batched eigvalss throws: the reference's NotSymmetric (catchable as
+// such, same what()), plus the index of the first record that failed the gate
+// -- the record on which a loop of scalar eigvalss calls would have thrown
+// (src/eigensolver.cpp:102).
+struct NotSymmetricAt : NotSymmetric {
+  std::size_t index;
+  explicit NotSymmetricAt(std::size_t i) : NotSymmetric(), index(i) {}
+};
+
 namespace batch_detail {
 inline void check(int rc) {
   if (rc == EIG33_OK) return;
   const std::string msg = eig33cu_last_error();
-  if (rc == EIG33_ENOTSYM) throw NotSymmetric{};
+  if (rc == EIG33_ENOTSYM) {
+    const long long i = eig33cu_last_notsym_index();
+    throw NotSymmetricAt(i < 0 ? 0 : static_cast<std::size_t>(i));
+  }
   if (rc == EIG33_EINVAL) throw std::invalid_argument(msg);
   throw CudaError(msg);
 }
@@ -107,7 +120,8 @@ inline void eigvals(const Mat3* a, std::size_t n, EigenTriple* out) {
   }
 }
 
-// Throws NotSymmetric if any record fails the gate (outputs of the others are written).
+// Throws NotSymmetricAt (a NotSymmetric) naming the first record that fails the
+// gate; the outputs of every other record are written.
 inline void eigvalss(const Mat3* a, std::size_t n, EigenTriple* out) {
   std::vector<double> lam(n * 3);
   std::vector<std::uint8_t> flags(n);

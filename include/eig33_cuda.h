@@ -42,6 +42,12 @@ extern "C" {
 int eig33cu_version(void);
 /* Thread-local description of the last failure ("" if none). */
 const char* eig33cu_last_error(void);
+/* Thread-local: index (within the batch) of the first record that failed the
+ * symmetry gate in the last eig33_eigvalss_host / eig33_multi_eigvalss call of
+ * this thread, or -1.  The reference's scalar eigvalss throws NotSymmetric for
+ * that record (src/eigensolver.cpp:102); the batch C++ wrapper rethrows it
+ * with this index (include/eig33/batch.hpp). */
+long long eig33cu_last_notsym_index(void);
 
 /* Batched eig33::invariants(a, AlgorithmVariant::Stable)
  * (reference include/eig33/invariants.hpp:74, src/invariants.cpp:76-85).
@@ -85,8 +91,11 @@ int eig33cu_disc_naive(const double* d_j2, const double* d_j3, size_t n, double*
                        void* stream);
 
 /* Synchronous host-buffer versions on one device (chunked, pipelined
- * H2D / kernel / D2H over 3 streams).  eig33_eigvalss_host returns
- * EIG33_ENOTSYM if any matrix failed the symmetry gate (outputs still written). */
+ * H2D / kernel / D2H over 3 streams; the calling thread's current device is
+ * restored on return).  eig33_eigvalss_host returns EIG33_ENOTSYM if any
+ * matrix failed the symmetry gate (outputs of all records still written;
+ * eig33cu_last_notsym_index() names the first).  On an error return every
+ * copy the call queued has completed: nothing writes caller memory later. */
 int eig33_invariants_host(const double* h_a, size_t n, double* h_inv, int device);
 /* invariants(a, variant) over host buffers, variant 0 Stable, 1 Naive, 2 NaiveTensor
  * (include/eig33/invariants.hpp:74, src/invariants.cpp:76-98). */
@@ -103,6 +112,10 @@ int eig33_eigvalss_host(const double* h_a, size_t n, double* h_inv, double* h_la
  * bitwise identical for every ngpu. */
 int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_lam,
                         uint8_t* h_flags, int ngpu);
+/* Same, with an explicit device per shard: shard g (same bounds, G = ndev)
+ * runs on devices[g]; a device may appear more than once. */
+int eig33_multi_eigvals_on(const double* h_a, size_t n, double* h_inv, double* h_lam,
+                           uint8_t* h_flags, const int* devices, int ndev);
 int eig33_multi_invariants(const double* h_a, size_t n, double* h_inv, int ngpu);
 int eig33_multi_eigvalss(const double* h_a, size_t n, double* h_inv, double* h_lam,
                          uint8_t* h_flags, int ngpu);

@@ -47,6 +47,7 @@ C_ABI_SYMBOLS = (
     "eig33cu_generate",
     "eig33cu_invariants_variant", "eig33cu_eigvals_naive", "eig33cu_jacobians",
     "eig33cu_generate_case", "eig33cu_disc_naive", "eig33_invariants_variant_host",
+    "eig33cu_last_notsym_index", "eig33_multi_eigvals_on",
 )
 VARIANTS = {"Stable": 0, "Naive": 1, "NaiveTensor": 2}  # reference AlgorithmVariant
 
@@ -84,6 +85,8 @@ def lib() -> ctypes.CDLL:
         "eig33cu_disc_naive": ([P, P, S, P, P], I),
         "eig33_invariants_variant_host": ([P, S, I, P, I], I),
         "eig33cu_generate_case": ([I, I, ctypes.c_double, P, S, P, P], I),
+        "eig33cu_last_notsym_index": ([], ctypes.c_longlong),
+        "eig33_multi_eigvals_on": ([P, S, P, P, P, P, I], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -366,15 +369,22 @@ def generate_case(path: str, transform: str, deltas, gamma: float = 1e-3, device
     return out
 
 
-def multi_eigvals(a, ngpu: int, *, return_invariants=False, return_flags=False) -> EigResult:
-    """Host batch sharded over devices 0..ngpu-1 (eig33_multi_eigvals)."""
+def multi_eigvals(a, ngpu: int = None, *, devices=None, return_invariants=False,
+                  return_flags=False) -> EigResult:
+    """Host batch sharded over devices 0..ngpu-1 (eig33_multi_eigvals), or over
+    an explicit per-shard device list (eig33_multi_eigvals_on)."""
     arr = _records_np(a)
     n = arr.shape[0]
     lam = np.empty((n, 3))
     inv = np.empty((n, 4)) if return_invariants else None
     flags = np.empty((n,), np.uint8) if return_flags else None
-    _check(lib().eig33_multi_eigvals(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(ngpu)),
-           "multi_eigvals")
+    if devices is not None:
+        d = np.ascontiguousarray(np.asarray(devices, dtype=np.int32).reshape(-1))
+        _check(lib().eig33_multi_eigvals_on(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), _ptr(d),
+                                            int(d.size)), "multi_eigvals")
+    else:
+        _check(lib().eig33_multi_eigvals(_ptr(arr), n, _ptr(inv), _ptr(lam), _ptr(flags), int(ngpu)),
+               "multi_eigvals")
     return EigResult(lam, inv, flags)
 
 

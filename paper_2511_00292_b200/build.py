@@ -5,6 +5,9 @@
   oracle/_ref/libeig33_ref.so           checker: compiled reference core (only
                                         when /root/reference is present)
   tests/hostmath/libhostmath.so         test harness: product math built for CPU
+  tools/probes/libeig33_probes.so       measurement probes for bench.py / tools
+                                        (FP64 issue rate, data-path energy);
+                                        never linked into the product
 
 Usage: python -m paper_2511_00292_b200.build [--product-only]
 """
@@ -27,7 +30,9 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
     "-Xptxas", "-v",
 ]
-SOURCES = ["eig33_kernels.cu", "eig33_gen.cu", "eig33_aux.cu", "eig33_host.cpp", "eig33_probe.cu"]
+SOURCES = ["eig33_kernels.cu", "eig33_gen.cu", "eig33_aux.cu", "eig33_host.cpp"]
+PROBES_SRC = os.path.join(ROOT, "tools", "probes", "eig33_probes.cu")
+PROBES_SO = os.path.join(ROOT, "tools", "probes", "libeig33_probes.so")
 
 
 def _nvcc():
@@ -57,7 +62,8 @@ def _stale(target, deps):
 
 def build_product(force=False):
     deps = [os.path.join(CSRC, s) for s in SOURCES] + [
-        os.path.join(CSRC, h) for h in ("eig33_math.cuh", "eig33_tables.h", "eig33_internal.h")
+        os.path.join(CSRC, h) for h in ("eig33_math.cuh", "eig33_tables.h", "eig33_internal.h",
+                                         "eig33_fused.cuh", "eig33_gen_core.h")
     ] + [os.path.join(ROOT, "include", "eig33_cuda.h")]
     if not force and not _stale(SO, deps):
         return SO
@@ -95,6 +101,18 @@ def build_variant(name, defines):
     return so
 
 
+def build_probes(force=False):
+    deps = [PROBES_SRC] + [os.path.join(CSRC, h) for h in ("eig33_math.cuh", "eig33_tables.h",
+                                                             "eig33_fused.cuh", "eig33_gen_core.h")]
+    if not force and not _stale(PROBES_SO, deps):
+        return PROBES_SO
+    tmp = PROBES_SO + ".tmp"
+    _run([_nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, PROBES_SRC],
+         log=os.path.join(os.path.dirname(PROBES_SO), "build.log"))
+    os.replace(tmp, PROBES_SO)
+    return PROBES_SO
+
+
 def build_oracle():
     make = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"]
     _run(make)
@@ -113,6 +131,7 @@ def build_hostmath():
 
 def build_all(force=False):
     build_product(force)
+    build_probes(force)
     build_oracle()
     build_hostmath()
 

@@ -1,0 +1,559 @@
+// eig33_fused.cuh -- device code of the batched eig33 hot path: the
+// persistent fused kernel k_fused, k_invariants, the deferred advisory and
+// k_triple_angle.  Included by eig33_kernels.cu (the
+// product: launch plumbing + device-pointer C ABI) and by the measurement
+// probes under tools/probes (the only place k_fused's MEMONLY form is
+// instantiated; the product library never contains it).
+//
+// MUST be compiled with --fmad=false: the invariant arithmetic is bit-exact
+// against the reference only without contraction (proj/src/CMakeLists.txt:9-10).
+// The includer defines EIG33_TABLE_DECL and includes eig33_tables.h first.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "eig33_math.cuh"
+#include "../../include/eig33_cuda.h"
+
+namespace eig33b {
+
+#ifndef EIG33_PDL
+#define EIG33_PDL 1
+#endif
+#ifndef EIG33_THREADS
+#define EIG33_THREADS 256
+#endif
+constexpr int kThreads = EIG33_THREADS;  // threads per block
+constexpr int kWarps = kThreads / 32;
+#ifndef EIG33_RPL
+#define EIG33_RPL 2
+#endif
+constexpr int kRPL = EIG33_RPL;  // records per lane per chunk (1, 2 or 4)
+static_assert(kRPL == 1 || kRPL == 2 || kRPL == 4, "kRPL must be 1, 2 or 4");
+constexpr int kChunk = 32 * kRPL;  // records per warp chunk
+#ifndef EIG33_STAGES
+#define EIG33_STAGES (4 / EIG33_RPL)
+#endif
+constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth (power of two)
+static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
+#ifndef EIG33_MIN_BLOCKS
+#define EIG33_MIN_BLOCKS 2
+#endif
+constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
+constexpr int kTabDoubles = EIG33_TAB_N;
+constexpr uint32_t kChunkBytes = kChunk * 9 * sizeof(double);  // 2304 * kRPL
+constexpr uint8_t kPending = 0x4;  // internal: advisory still to be evaluated
+
+enum Mode { kEig = 0, kInv = 1, kSym = 2 };
+
+struct __align__(16) Smem {
+  double in[kWarps][kStages][kChunk * 9];
+  double tab[kTabDoubles + 7];
+  unsigned long long bar[kWarps][kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
+// Programmatic dependent launch: k_fused / k_invariants are launched with
+// programmatic stream serialisation, so their blocks may start while the
+// previous kernel on the stream drains.  Everything before pdl_wait() touches
+// only SMEM (barrier init, table copy from a read-only global array); every
+// read or write of caller buffers comes after it, and griddepcontrol.wait
+// returns only once the previous grid has completed and its writes are
+// visible.  pdl_trigger() lets the next kernel do the same.
+__device__ __forceinline__ void pdl_trigger() {
+#if EIG33_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if EIG33_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+__device__ __forceinline__ void load_tables(double* tab) {
+  copy_table(tab, eig33_tab);
+}
+
+struct Tabs {
+  const double* tab;
+};
+
+// The checked reference-order kernels return the same bits as the moderate
+// ones on moderate records, so a warp with any non-moderate lane runs the
+// checked kernel on every lane rather than both kernels one after the other
+// (divergent lanes would serialise them).  `mask`: the lanes executing the call.
+__device__ __forceinline__ Inv invariants_warp(const double m[9], bool mod, unsigned mask) {
+  return __all_sync(mask, mod) ? invariants_moderate(m) : invariants(m);
+}
+
+// Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
+// the eigen-stage carry.  Moderate records (every |a_ij| in [2^-100,2^100), the
+// common case) use the CSE DAG; the rest the checked reference-order kernel.
+// Both produce the reference's bits.
+template <int MODE, bool WANT_FLAGS>
+__device__ __forceinline__ void stage1(double m[9], bool& mod, Inv& v, Carry& c, uint8_t& f,
+                                       bool& bad) {
+  f = 0;
+  bad = false;
+  if (MODE == kSym) {
+    if (not_symmetric(m)) {
+      bad = true;
+      mod = false;
+      f = EIG33_FLAG_NOT_SYMMETRIC;
+    }
+    m[3] = m[1];  // mirror the upper triangle, src/eigensolver.cpp:108-111
+    m[6] = m[2];
+    m[7] = m[5];
+  }
+  v = invariants_warp(m, mod, 0xffffffffu);
+  if (MODE == kSym && bad) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    v.i1 = v.j2 = v.j3 = v.disc = qnan;
+  }
+  if (MODE == kEig && WANT_FLAGS && v.disc < 0.0) f = kPending;
+  c = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+}
+
+// Stage 2 (eigenvalues) of a record from its carry, general form; called by
+// whole warps.  As in invariants_warp, the checked from_invariants serves every
+// lane once any lane needs it (same bits on moderate carries).
+__device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const Tabs& T) {
+  Lam L;
+  if (__all_sync(0xffffffffu, mod || bad)) {
+    L = eig_moderate_bl(c, T.tab);
+  } else {
+    const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
+    L = from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
+  }
+  if (bad) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    L = Lam{qnan, qnan, qnan};
+  }
+  return L;
+}
+
+// Slow tiers of the record pipeline.  The general tier is a real call so that
+// its register demand never enters the allocation of the steady-state loop
+// (inlining it made ptxas move arrays to local memory there and cost 3x); the
+// moderate tier is small enough to inline.
+struct M9 {
+  double e[9];
+};
+struct StepOut {
+  Lam L;
+  Inv v;
+  uint8_t f;
+  bool bad, mod;
+};
+
+// Tier B, warp-uniform: every lane moderate but some carried record has
+// j2 <= 0 or disc <= 0: branch-free eig_moderate_bl interleaved with the DAG.
+// Inlined: measured +6% on config 4 (every warp step here) and +1.3% on the
+// sustained config-3 bench against an out-of-line call (argument moves, no
+// overlap with the loads/stores around the call).
+template <int MODE, bool WANT_FLAGS>
+__device__ __forceinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* tab) {
+  StepOut o;
+  o.L = eig_moderate_bl(pc, tab);
+  o.v = invariants_moderate(mm.e);
+  o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
+  o.bad = false;
+  o.mod = true;
+  return o;
+}
+
+// Tier C, per lane: the checked reference-order path (zeros, subnormals,
+// extreme exponents, inf/NaN, eigvalss rejects).
+template <int MODE, bool WANT_FLAGS>
+__device__ __noinline__ StepOut tier_general(M9 mm, bool sym_ok, bool mod, Carry pc, bool pmod,
+                                             bool pbad, const double* tab) {
+  StepOut o;
+  o.L = stage2(pc, pmod, pbad, Tabs{tab});
+  if (MODE == kSym) {
+    o.bad = !sym_ok;  // already mirrored: the gate verdict decides
+    o.f = o.bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
+    o.mod = mod && !o.bad;
+    // rejected lanes do not vote: their (garbage) invariants are replaced by NaN
+    o.v = invariants_warp(mm.e, mod || o.bad, 0xffffffffu);
+    if (o.bad) {
+      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+      o.v.i1 = o.v.j2 = o.v.j3 = o.v.disc = qnan;
+    }
+  } else {
+    Carry nc;
+    bool m2 = mod;
+    stage1<MODE, WANT_FLAGS>(mm.e, m2, o.v, nc, o.f, o.bad);
+    o.mod = m2;
+  }
+  return o;
+}
+
+// Per-warp record pipeline.  Work unit = a chunk of 32 consecutive records,
+// one per lane.  Lane 0 streams the warp's chunks HBM -> SMEM with
+// cp.async.bulk into a kStages-deep per-warp ring completed on per-warp
+// mbarriers: no block-wide barrier in the loop.
+struct WarpRing {
+  double* ring;
+  unsigned long long* bars;
+  const double* a;
+  long long n, nchunks, full, W;
+  int lane;
+};
+
+template <bool TMA>
+__device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
+  if (TMA && R.lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const long long c = gw + (long long)s * R.W;
+      if (c < R.full) {
+        mbar_expect_tx(&R.bars[s], kChunkBytes);
+        EIG33_CHECK((c + 1) * kChunk <= R.n);
+        bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+      }
+    }
+  }
+}
+
+// Chunk c (iteration it) of this warp: wait for its TMA (or load it
+// cooperatively: misaligned input / ragged last chunk); returns the SMEM
+// buffer and the record count.
+template <bool TMA>
+__device__ __forceinline__ double* ring_acquire(const WarpRing& R, long long c, uint32_t it,
+                                                int& cnt) {
+  const uint32_t stage = it & (kStages - 1);
+  double* buf = R.ring + stage * (kChunk * 9);
+  cnt = kChunk;
+  if (TMA && c < R.full) {
+    mbar_wait(&R.bars[stage], (it / kStages) & 1u);
+  } else {
+    const long long base = c * kChunk;
+    cnt = (int)min((long long)kChunk, R.n - base);
+    const double* src = R.a + base * 9;
+#pragma unroll
+    for (int j = 0; j < 9 * kRPL; ++j) {
+      const int e = R.lane + 32 * j;
+      buf[e] = e < cnt * 9 ? __ldg(src + e) : 1.0;
+    }
+    __syncwarp();
+  }
+  return buf;
+}
+// Record h (0..kRPL-1) of this lane from the chunk buffer; `mod` consumes all
+// nine loads, so once every record of the chunk is read the stage can be
+// handed back to the TMA engine (ring_release).
+__device__ __forceinline__ void ring_read(const double* buf, int lane, int h, double m[9],
+                                          bool& mod) {
+#pragma unroll
+  for (int j = 0; j < 9; ++j) m[j] = buf[(lane + 32 * h) * 9 + j];
+  mod = is_moderate(m);
+  if (!mod) mod = is_moderate_or_zero(m);
+}
+template <bool TMA>
+__device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
+                                             double* buf) {
+  __syncwarp();
+  if (TMA && R.lane == 0) {
+    const uint32_t stage = it & (kStages - 1);
+    const long long nc = c + (long long)kStages * R.W;
+    if (nc < R.full) {
+      mbar_expect_tx(&R.bars[stage], kChunkBytes);
+      EIG33_CHECK((nc + 1) * kChunk <= R.n);
+      bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
+    }
+  }
+}
+
+// Persistent fused kernel, software-pipelined across records: iteration i
+// computes the invariants of chunk i and the eigenvalue stage of chunk i-1 in
+// one basic block (both branch-free in the moderate case), so the long serial
+// transcendental chain of one record overlaps the wide invariant DAG of the
+// next.  Outputs go straight from registers to HBM (a warp's lambda stores
+// cover one contiguous 768-B run; L2 merges the sectors).
+// MEMONLY (measurement probe eig33_probe_memonly only): the same ring, tier
+// tests and stores with the steady-state arithmetic removed -- the kernel's own
+// data-movement energy for the energy roof in bench.py.
+template <int MODE, bool TMA, bool WANT_INV, bool WANT_FLAGS, bool MEMONLY = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_fused(const double* __restrict__ a, long long n, double* __restrict__ inv,
+            double* __restrict__ lam, uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
+             (long long)gridDim.x * kWarps, lane};
+
+  if (TMA && lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_trigger();
+  load_tables(S.tab);
+  __syncthreads();  // tables + barrier init; the only block-wide barrier
+  pdl_wait();
+  const Tabs T{S.tab};
+  ring_prologue<TMA>(R, gw);
+  if (gw >= R.nchunks) return;
+
+  double m[9];
+  bool mod, bad, pmod, pbad, pfast, pvalid;
+  Inv v;
+  Carry pc;
+  uint8_t f;
+  long long pr;  // record index of the carried stage
+  auto store_stage1 = [&](long long r, bool valid) {
+    if (!valid) return;
+    EIG33_CHECK(r >= 0 && r < R.n);
+    if (WANT_INV) {
+      inv[r * 4 + 0] = v.i1;
+      inv[r * 4 + 1] = v.j2;
+      inv[r * 4 + 2] = v.j3;
+      inv[r * 4 + 3] = v.disc;
+    }
+    if (MODE != kInv && WANT_FLAGS) flags[r] = f;
+  };
+  auto store_lam = [&](const Lam& L) {
+    if (!pvalid) return;
+    EIG33_CHECK(pr >= 0 && pr < R.n);
+    lam[pr * 3 + 0] = L.l1;
+    lam[pr * 3 + 1] = L.l2;
+    lam[pr * 3 + 2] = L.l3;
+  };
+  // One step of the record pipeline: stage 2 of the carried record, stage 1 of m.
+  auto step = [&](long long r, bool valid) {
+    Carry nc;
+    Lam L;
+    bool sym_ok = true;
+    if (MODE == kSym) {
+      // eigvalss gate + mirror (src/eigensolver.cpp:98-111) ahead of the
+      // steady-state test; mirroring keeps a moderate record moderate.
+      sym_ok = !not_symmetric(m);
+      m[3] = m[1];
+      m[6] = m[2];
+      m[7] = m[5];
+    }
+    // Warp-uniform tier choice, so a warp never runs two tiers for one step.
+    if (__all_sync(0xffffffffu, sym_ok && mod && pfast)) {
+      // steady state: one branch-free block (stage 2 of pr, stage 1 of r);
+      // the long transcendental chain is written first so the scheduler
+      // starts it early and fills its latency with the invariant DAG.
+      if constexpr (MEMONLY) {  // measurement probe: same data movement, no arithmetic
+        L = Lam{pc.a0, pc.a4, pc.a8};
+        v = Inv{m[0], 1.0, m[1], 1.0};
+      } else {
+        L = eig_fast(pc, T.tab);
+        v = invariants_moderate(m);
+      }
+      if (MODE == kEig && WANT_FLAGS) f = v.disc < 0.0 ? kPending : 0;
+      if (MODE == kSym) f = 0;
+      bad = false;
+    } else {
+      M9 mm;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) mm.e[k] = m[k];
+      StepOut o;
+      if (__all_sync(0xffffffffu, sym_ok && mod && pmod))
+        o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
+      else
+        o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pmod, pbad, T.tab);
+      L = o.L;
+      v = o.v;
+      f = o.f;
+      bad = o.bad;
+      mod = o.mod;
+    }
+    nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+    store_lam(L);
+    store_stage1(r, valid);
+    pc = nc;
+    pmod = mod;
+    pfast = mod && fast_carry(v);
+    pbad = bad;
+    pr = r;
+    pvalid = valid;
+  };
+
+  // ---- prologue: first chunk; stage 1 of its first record ----
+  int cnt;
+  double* buf = ring_acquire<TMA>(R, gw, 0, cnt);
+  ring_read(buf, lane, 0, m, mod);
+  if (kRPL == 1) ring_release<TMA>(R, gw, 0, buf);
+  stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
+  pmod = mod;
+  pfast = mod && fast_carry(v);
+  pr = gw * kChunk + lane;
+  pvalid = lane < cnt;
+  store_stage1(pr, pvalid);
+#pragma unroll
+  for (int h = 1; h < kRPL; ++h) {
+    ring_read(buf, lane, h, m, mod);
+    if (h == kRPL - 1) ring_release<TMA>(R, gw, 0, buf);
+    step(gw * kChunk + 32 * h + lane, 32 * h + lane < cnt);
+  }
+
+  uint32_t it = 1;
+  for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
+    buf = ring_acquire<TMA>(R, c, it, cnt);
+    const long long base = c * kChunk + lane;
+#pragma unroll
+    for (int h = 0; h < kRPL; ++h) {
+      ring_read(buf, lane, h, m, mod);
+      if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
+      step(base + 32 * h, 32 * h + lane < cnt);
+    }
+  }
+  store_lam(stage2(pc, pmod, pbad, T));
+}
+
+// Invariants-only kernel: stage 1 alone, same per-warp TMA ring.
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_invariants(const double* __restrict__ a, long long n, double* __restrict__ inv,
+                 double* /*lam: unused*/, uint8_t* /*flags: unused*/) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
+             (long long)gridDim.x * kWarps, lane};
+  if (TMA && lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_trigger();
+  __syncthreads();
+  pdl_wait();
+  ring_prologue<TMA>(R, gw);
+  uint32_t it = 0;
+  for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
+    int cnt;
+    double* buf = ring_acquire<TMA>(R, c, it, cnt);
+#pragma unroll
+    for (int h = 0; h < kRPL; ++h) {
+      double m[9];
+      bool mod;
+      ring_read(buf, lane, h, m, mod);
+      if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
+      const Inv v = invariants_warp(m, mod, 0xffffffffu);
+      if (lane + 32 * h < cnt) {
+        const long long r = c * kChunk + 32 * h + lane;
+        inv[r * 4 + 0] = v.i1;
+        inv[r * 4 + 1] = v.j2;
+        inv[r * 4 + 2] = v.j3;
+        inv[r * 4 + 3] = v.disc;
+      }
+    }
+  }
+}
+
+// Deferred advisory: evaluate src/eigensolver.cpp:54 only where k_fused found
+// disc < 0.  A block takes a window of kThreads*16 records: each thread reads
+// its 16 flag bytes with one 16-B load, and a window with nothing pending is
+// dismissed by one __syncthreads_or (the common case costs one coalesced read
+// of the flags).  Otherwise the pending records are compacted into SMEM
+// (warp scan of per-thread counts) and the block works the list densely.
+constexpr int kAdvWindow = kThreads * 16;
+__global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict__ a, long long n,
+                                                       const double* __restrict__ inv,
+                                                       uint8_t* __restrict__ flags) {
+  __shared__ int list[kAdvWindow];
+  __shared__ int wsum[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = ((uintptr_t)flags & 15u) == 0;
+  constexpr uint64_t kPend8 = 0x0101010101010101ull * kPending;
+  for (long long w0 = (long long)blockIdx.x * kAdvWindow; w0 < n;
+       w0 += (long long)gridDim.x * kAdvWindow) {
+    const long long base = w0 + 16LL * threadIdx.x;
+    uint64_t w[2] = {0, 0};
+    if (vec && base + 16 <= n) {
+      const ulonglong2 v2 = __ldcg(reinterpret_cast<const ulonglong2*>(flags + base));
+      w[0] = v2.x;
+      w[1] = v2.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (base + k < n) w[k >> 3] |= (uint64_t)flags[base + k] << (8 * (k & 7));
+    }
+    const uint64_t pm0 = w[0] & kPend8, pm1 = w[1] & kPend8;
+    if (!__syncthreads_or((pm0 | pm1) != 0)) continue;
+    const int cnt = __popcll(pm0) + __popcll(pm1);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int pos = incl - cnt, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const int sw = wsum[w];
+      pos += w < warp ? sw : 0;
+      total += sw;
+    }
+    for (uint64_t r = pm0; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + ((__ffsll((long long)r) - 1) >> 3);
+    for (uint64_t r = pm1; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + 8 + ((__ffsll((long long)r) - 1) >> 3);
+    __syncthreads();
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const long long idx = w0 + list[j];
+      double m[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
+      Inv v;
+      if (inv) {  // k_fused already wrote this record's invariants
+        v = Inv{inv[idx * 4], inv[idx * 4 + 1], inv[idx * 4 + 2], inv[idx * 4 + 3]};
+      } else {
+        const bool mod = is_moderate(m) || is_moderate_or_zero(m);
+        v = invariants_warp(m, mod, __activemask());  // same bits either way
+      }
+      flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
+    }
+    __syncthreads();  // list and wsum are reused by the next window
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_triple_angle(const double* __restrict__ j3,
+                                                           const double* __restrict__ disc,
+                                                           long long n, double* __restrict__ phi) {
+  __shared__ __align__(16) double tab[kTabDoubles + 7];
+  load_tables(tab);
+  __syncthreads();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    phi[i] = triple_angle(j3[i], disc[i], tab);
+}
+
+}  // namespace eig33b

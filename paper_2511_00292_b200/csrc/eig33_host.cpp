@@ -84,34 +84,21 @@ int ensure(Staging& s, size_t cap) {
 // Page-locking a caller's pageable buffer per call (cudaHostRegister +
 // Unregister) measured slower than the driver's staged pageable copies at every
 // size (1 record: 1.1 ms vs 31 us; 2^22 records: 55 vs 48 ms, tools/call_latency.py),
-// so by default it is not done; EIG33_PIN_MIN_BYTES=<bytes> re-enables it above
-// that size (measurement).  Buffers the caller already pinned are used directly.
-size_t pin_min_bytes() {
-  static const size_t v = [] {
-    const char* e = getenv("EIG33_PIN_MIN_BYTES");
-    return e ? (size_t)strtoull(e, nullptr, 10) : ~size_t(0);
-  }();
-  return v;
-}
+// so it is never done: buffers the caller already pinned are DMA'd directly,
+// large pageable ones go through the pinned bounce buffers of run_staged.
 
-// Page-lock a host range for the duration of a call unless it already is.
-struct PinGuard {
-  void* p = nullptr;
-  bool registered = false;
-  PinGuard(const void* ptr, size_t bytes) {
-    if (!ptr || !bytes || bytes < pin_min_bytes()) return;
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost) return;
-    cudaGetLastError();
-    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterPortable) == cudaSuccess) {
-      p = const_cast<void*>(ptr);
-      registered = true;
-    } else {
-      cudaGetLastError();  // fall back to pageable copies
+// Restores the calling thread's current device on every return path (the
+// host entry points switch to the requested device).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
     }
   }
-  ~PinGuard() {
-    if (registered) cudaHostUnregister(p);
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
   }
 };
 
@@ -128,8 +115,13 @@ bool is_pinned(const void* p) {
 }
 
 // Parallel memcpy for the staged (pageable-buffer) pipeline: a persistent pool
-// of host threads splits a copy into 4 MB parts; the calling thread works too.
-// One copy at a time (calls are serialised); never destroyed (threads parked).
+// of host threads splits each copy into 4 MB parts; the calling thread works on
+// its own copy too.  Several copies may be in flight at once (the multi-GPU
+// driver runs one host thread per device): each copy is a Job with its own
+// counters, idle workers join any job that still has unclaimed parts, and a
+// copy returns only after every part is done AND no worker still holds a
+// reference to its Job (so a slow worker can never touch a finished job's
+// state or the next job's buffers).  Never destroyed (threads parked).
 class CopyPool {
  public:
   static CopyPool& get() {
@@ -141,61 +133,82 @@ class CopyPool {
       std::memcpy(dst, src, bytes);
       return;
     }
-    std::lock_guard<std::mutex> one(call_mu_);
+    Job j;
+    j.dst = static_cast<char*>(dst);
+    j.src = static_cast<const char*>(src);
+    j.bytes = bytes;
+    j.nparts = (bytes + kPart - 1) / kPart;
     {
       std::lock_guard<std::mutex> g(mu_);
-      dst_ = static_cast<char*>(dst);
-      src_ = static_cast<const char*>(src);
-      bytes_ = bytes;
-      nparts_ = (bytes + kPart - 1) / kPart;
-      finished_.store(0);
-      next_.store(0);
-      ++gen_;
+      jobs_.push_back(&j);
     }
     cv_.notify_all();
-    run_parts();
+    run(j);
     std::unique_lock<std::mutex> g(mu_);
-    done_cv_.wait(g, [&] { return finished_.load() == nparts_; });
+    done_cv_.wait(g, [&] { return j.done.load() == j.nparts && j.refs == 0; });
+    unlink(&j);
   }
 
  private:
   static constexpr size_t kPart = size_t(4) << 20;
+  struct Job {
+    char* dst = nullptr;
+    const char* src = nullptr;
+    size_t bytes = 0, nparts = 0;
+    std::atomic<size_t> next{0}, done{0};
+    int refs = 0;  // workers inside run(); guarded by mu_
+  };
   CopyPool() {
     const unsigned hw = std::thread::hardware_concurrency();
-    nworkers_ = hw > 1 ? std::min(hw, 16u) - 1 : 0;
+    nworkers_ = hw > 1 ? std::min(hw, 32u) - 1 : 0;
     for (unsigned i = 0; i < nworkers_; ++i) std::thread([this] { work(); }).detach();
   }
-  void run_parts() {
+  void run(Job& j) {
     for (;;) {
-      const size_t i = next_.fetch_add(1);
-      if (i >= nparts_) return;
-      const size_t off = i * kPart, len = std::min(kPart, bytes_ - off);
-      std::memcpy(dst_ + off, src_ + off, len);
-      if (finished_.fetch_add(1) + 1 == nparts_) {
+      const size_t i = j.next.fetch_add(1);
+      if (i >= j.nparts) return;
+      const size_t off = i * kPart, len = std::min(kPart, j.bytes - off);
+      std::memcpy(j.dst + off, j.src + off, len);
+      if (j.done.fetch_add(1) + 1 == j.nparts) {
         std::lock_guard<std::mutex> g(mu_);
         done_cv_.notify_all();
       }
     }
   }
+  // first listed job with unclaimed parts (mu_ held)
+  Job* pick() {
+    for (Job* j : jobs_)
+      if (j->next.load() < j->nparts) return j;
+    return nullptr;
+  }
+  void unlink(Job* j) {  // mu_ held
+    for (size_t k = 0; k < jobs_.size(); ++k)
+      if (jobs_[k] == j) {
+        jobs_.erase(jobs_.begin() + (long)k);
+        return;
+      }
+  }
   void work() {
-    unsigned long long seen = 0;
     for (;;) {
+      Job* j;
       {
         std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [&] { return gen_ != seen; });
-        seen = gen_;
+        cv_.wait(g, [&] { return pick() != nullptr; });
+        j = pick();
+        ++j->refs;
       }
-      run_parts();
+      run(*j);
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        --j->refs;
+      }
+      done_cv_.notify_all();
     }
   }
   unsigned nworkers_ = 0;
-  std::mutex call_mu_, mu_;
+  std::mutex mu_;
   std::condition_variable cv_, done_cv_;
-  char* dst_ = nullptr;
-  const char* src_ = nullptr;
-  size_t bytes_ = 0, nparts_ = 0;
-  std::atomic<size_t> next_{0}, finished_{0};
-  unsigned long long gen_ = 0;
+  std::vector<Job*> jobs_;
 };
 
 // Pinned host bounce buffers (per device, grown on demand) for callers whose
@@ -257,6 +270,22 @@ int launch_op(Op op, const double* d_a, size_t cnt, double* d_inv, double* d_lam
   return EIG33_EINVAL;
 }
 
+// Waits for everything queued on the device's three pipeline streams; used on
+// every error return so that no async copy can still write a caller buffer
+// (or read a staging buffer) after the call has returned.
+void drain(Staging& s) {
+  for (int i = 0; i < kSets; ++i)
+    if (s.st[i]) cudaStreamSynchronize(s.st[i]);
+  cudaGetLastError();
+}
+
+// Index of the first record whose flag byte carries NotSymmetric, or -1.
+long long first_notsym(const uint8_t* flags, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (flags[i] & EIG33_FLAG_NOT_SYMMETRIC) return (long long)i;
+  return -1;
+}
+
 // Staged pipeline: chunk c goes caller -> pinned in[b] (pool copy) -> device
 // (H2D) -> kernel -> pinned out[b] (D2H) -> caller (pool copy), b = c % kSets;
 // the host copies of chunk c overlap the device work of chunks c-1, c-2.
@@ -307,42 +336,15 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
   return EIG33_OK;
 }
 
-int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
-               int device, bool* any_notsym) {
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaSetDevice", e);
-  if (n == 0) return EIG33_OK;
-  if (device < 0 || device >= 64) return fail(EIG33_EINVAL, "device index out of range");
-  Staging& s = g_stage[device];
-  std::lock_guard<std::mutex> lock(s.mu);
-  const bool want_flags = h_flags != nullptr || op == Op::Sym;
-  std::vector<uint8_t> local_flags;
-  uint8_t* flags_out = h_flags;
-  if (op == Op::Sym && !h_flags) {
-    local_flags.resize(n);
-    flags_out = local_flags.data();
-  }
-  int rc;
-  // Caller buffers that are pageable and large go through pinned bounce
-  // buffers with parallel host copies; pinned ones are DMA'd directly.
-  const bool pinned = is_pinned(h_a) && is_pinned(h_inv) && is_pinned(h_lam) && is_pinned(h_flags);
-  if (!pinned && n * 9 * sizeof(double) >= kStageMinBytes && pin_min_bytes() == ~size_t(0)) {
-    rc = run_staged(op, s, h_a, n, h_inv, h_lam, flags_out, want_flags, device);
-    if (rc) return rc;
-    if (op == Op::Sym && any_notsym) {
-      bool any = false;
-      for (size_t i = 0; i < n && !any; ++i) any = (flags_out[i] & EIG33_FLAG_NOT_SYMMETRIC) != 0;
-      *any_notsym = any;
-    }
-    return EIG33_OK;
-  }
+// Direct pipeline over caller buffers (pinned, or small pageable ones the
+// driver stages itself): H2D of chunk c+1, kernel of chunk c and D2H of chunk
+// c-1 overlap on the three streams.
+int run_direct(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, double* h_lam,
+               uint8_t* flags_out, bool want_flags) {
   const size_t chunk = n < kChunk ? ((n + 1) & ~size_t(1)) : kChunk;
-  rc = ensure(s, chunk);
+  int rc = ensure(s, chunk);
   if (rc) return rc;
-  PinGuard pa(h_a, n * 9 * sizeof(double));
-  PinGuard pi(h_inv, h_inv ? n * 4 * sizeof(double) : 0);
-  PinGuard pl(h_lam, h_lam ? n * 3 * sizeof(double) : 0);
-  PinGuard pf(h_flags, h_flags ? n : 0);
+  cudaError_t e;
   const size_t nchunks = (n + chunk - 1) / chunk;
   for (size_t c = 0; c < nchunks; ++c) {
     const int b = int(c % kSets);
@@ -371,52 +373,112 @@ int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam,
     e = cudaStreamSynchronize(s.st[i]);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "stream sync", e);
   }
-  if (op == Op::Sym && any_notsym) {
-    bool any = false;
-    for (size_t i = 0; i < n && !any; ++i) any = (flags_out[i] & EIG33_FLAG_NOT_SYMMETRIC) != 0;
-    *any_notsym = any;
+  return EIG33_OK;
+}
+
+// One device, synchronous.  *notsym (eigvalss) receives the first record that
+// failed the symmetry gate, or -1.  The caller's current device is restored.
+int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
+               int device, long long* notsym) {
+  if (notsym) *notsym = -1;
+  if (n == 0) return EIG33_OK;
+  if (device < 0 || device >= 64) return fail(EIG33_EINVAL, "device index out of range");
+  DeviceGuard keep;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaSetDevice", e);
+  Staging& s = g_stage[device];
+  std::lock_guard<std::mutex> lock(s.mu);
+  const bool want_flags = h_flags != nullptr || op == Op::Sym;
+  std::vector<uint8_t> local_flags;
+  uint8_t* flags_out = h_flags;
+  if (op == Op::Sym && !h_flags) {
+    local_flags.resize(n);
+    flags_out = local_flags.data();
   }
+  // Caller buffers that are pageable and large go through pinned bounce
+  // buffers with parallel host copies; pinned ones are DMA'd directly.
+  const bool pinned = is_pinned(h_a) && is_pinned(h_inv) && is_pinned(h_lam) && is_pinned(h_flags);
+  const int rc = (!pinned && n * 9 * sizeof(double) >= kStageMinBytes)
+                     ? run_staged(op, s, h_a, n, h_inv, h_lam, flags_out, want_flags, device)
+                     : run_direct(op, s, h_a, n, h_inv, h_lam, flags_out, want_flags);
+  if (rc) {
+    drain(s);
+    return rc;
+  }
+  if (op == Op::Sym && notsym) *notsym = first_notsym(flags_out, n);
   return EIG33_OK;
 }
 
 // Contiguous even-aligned shards, one host thread and device each;
 // no exchange between devices.  Pageable buffers go through each device's
-// staged pipeline (the host copy pool is shared); pinned ones are DMA'd directly.
+// staged pipeline (the host copy pool serves all devices at once); pinned ones
+// are DMA'd directly.  `devices` lists the device of each shard (a device may
+// repeat: its shards then take turns on its pipeline).
 int run_multi(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
-              int ngpu, bool* any_notsym) {
+              const int* devices, int ndev, long long* notsym) {
+  if (notsym) *notsym = -1;
   int have = 0;
   cudaError_t e = cudaGetDeviceCount(&have);
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDeviceCount", e);
-  if (ngpu < 1 || ngpu > have) return fail(EIG33_EINVAL, "ngpu out of range");
-  std::vector<int> rcs(ngpu, 0);
-  std::vector<char> anys(ngpu, 0);
-  std::vector<std::string> errs(ngpu);
+  if (ndev < 1 || ndev > 64) return fail(EIG33_EINVAL, "ngpu out of range");
+  for (int g = 0; g < ndev; ++g)
+    if (devices[g] < 0 || devices[g] >= have) return fail(EIG33_EINVAL, "device index out of range");
+  std::vector<int> rcs(ndev, 0);
+  std::vector<long long> bad(ndev, -1);
+  std::vector<std::string> errs(ndev);
   std::vector<std::thread> th;
-  for (int g = 0; g < ngpu; ++g) {
-    const size_t lo = 2 * ((size_t)g * n / (2 * (size_t)ngpu));
-    const size_t hi = g + 1 == ngpu ? n : 2 * ((size_t)(g + 1) * n / (2 * (size_t)ngpu));
-    th.emplace_back([=, &rcs, &errs, &anys] {
-      bool any = false;
+  std::vector<size_t> los(ndev);
+  for (int g = 0; g < ndev; ++g) {
+    const size_t lo = 2 * ((size_t)g * n / (2 * (size_t)ndev));
+    const size_t hi = g + 1 == ndev ? n : 2 * ((size_t)(g + 1) * n / (2 * (size_t)ndev));
+    los[g] = lo;
+    const int dev = devices[g];
+    th.emplace_back([=, &rcs, &errs, &bad] {
       rcs[g] = run_device(op, h_a + lo * 9, hi - lo, h_inv ? h_inv + lo * 4 : nullptr,
-                          h_lam ? h_lam + lo * 3 : nullptr, h_flags ? h_flags + lo : nullptr, g,
-                          any_notsym ? &any : nullptr);
-      anys[g] = any;
+                          h_lam ? h_lam + lo * 3 : nullptr, h_flags ? h_flags + lo : nullptr, dev,
+                          notsym ? &bad[g] : nullptr);
       if (rcs[g]) errs[g] = eig33cu_last_error();
     });
   }
   for (auto& t : th) t.join();
-  for (int g = 0; g < ngpu; ++g)
-    if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
-  if (any_notsym) {
-    *any_notsym = false;
-    for (int g = 0; g < ngpu; ++g) *any_notsym = *any_notsym || anys[g];
-  }
+  for (int g = 0; g < ndev; ++g)
+    if (rcs[g]) return fail(rcs[g], "shard " + std::to_string(g) + " (device " + std::to_string(devices[g]) +
+                                        "): " + errs[g]);
+  if (notsym)
+    for (int g = 0; g < ndev; ++g)
+      if (bad[g] >= 0) {
+        *notsym = (long long)los[g] + bad[g];
+        break;
+      }
   return EIG33_OK;
+}
+
+int run_multi_n(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
+                int ngpu, long long* notsym) {
+  if (ngpu < 1 || ngpu > 64) return fail(EIG33_EINVAL, "ngpu out of range");
+  int have = 0;
+  cudaError_t e = cudaGetDeviceCount(&have);
+  if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDeviceCount", e);
+  if (ngpu > have) return fail(EIG33_EINVAL, "ngpu out of range");
+  std::vector<int> devs(ngpu);
+  for (int g = 0; g < ngpu; ++g) devs[g] = g;
+  return run_multi(op, h_a, n, h_inv, h_lam, h_flags, devs.data(), ngpu, notsym);
+}
+
+thread_local long long g_notsym = -1;
+
+int notsym_status(long long first) {
+  g_notsym = first;
+  if (first < 0) return EIG33_OK;
+  return fail(EIG33_ENOTSYM, "matrix is not symmetric to working accuracy (first at record " +
+                                 std::to_string(first) + ")");
 }
 
 }  // namespace
 
 extern "C" {
+
+long long eig33cu_last_notsym_index(void) { return g_notsym; }
 
 int eig33_invariants_host(const double* h_a, size_t n, double* h_inv, int device) {
   eig33b::set_error("");
@@ -443,34 +505,44 @@ int eig33_eigvals_host(const double* h_a, size_t n, double* h_inv, double* h_lam
 int eig33_eigvalss_host(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
                         int device) {
   eig33b::set_error("");
+  g_notsym = -1;
   if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_eigvalss_host: null pointer");
-  bool any = false;
-  const int rc = run_device(Op::Sym, h_a, n, h_inv, h_lam, h_flags, device, &any);
+  long long first = -1;
+  const int rc = run_device(Op::Sym, h_a, n, h_inv, h_lam, h_flags, device, &first);
   if (rc) return rc;
-  return any ? fail(EIG33_ENOTSYM, "matrix is not symmetric to working accuracy") : EIG33_OK;
+  return notsym_status(first);
 }
 
 int eig33_multi_eigvals(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
                         int ngpu) {
   eig33b::set_error("");
   if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_multi_eigvals: null pointer");
-  return run_multi(Op::Eig, h_a, n, h_inv, h_lam, h_flags, ngpu, nullptr);
+  return run_multi_n(Op::Eig, h_a, n, h_inv, h_lam, h_flags, ngpu, nullptr);
+}
+
+int eig33_multi_eigvals_on(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
+                           const int* devices, int ndev) {
+  eig33b::set_error("");
+  if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_multi_eigvals_on: null pointer");
+  if (!devices) return fail(EIG33_EINVAL, "eig33_multi_eigvals_on: null device list");
+  return run_multi(Op::Eig, h_a, n, h_inv, h_lam, h_flags, devices, ndev, nullptr);
 }
 
 int eig33_multi_invariants(const double* h_a, size_t n, double* h_inv, int ngpu) {
   eig33b::set_error("");
   if (n && (!h_a || !h_inv)) return fail(EIG33_EINVAL, "eig33_multi_invariants: null pointer");
-  return run_multi(Op::Inv, h_a, n, h_inv, nullptr, nullptr, ngpu, nullptr);
+  return run_multi_n(Op::Inv, h_a, n, h_inv, nullptr, nullptr, ngpu, nullptr);
 }
 
 int eig33_multi_eigvalss(const double* h_a, size_t n, double* h_inv, double* h_lam, uint8_t* h_flags,
                          int ngpu) {
   eig33b::set_error("");
+  g_notsym = -1;
   if (n && (!h_a || !h_lam)) return fail(EIG33_EINVAL, "eig33_multi_eigvalss: null pointer");
-  bool any = false;
-  const int rc = run_multi(Op::Sym, h_a, n, h_inv, h_lam, h_flags, ngpu, &any);
+  long long first = -1;
+  const int rc = run_multi_n(Op::Sym, h_a, n, h_inv, h_lam, h_flags, ngpu, &first);
   if (rc) return rc;
-  return any ? fail(EIG33_ENOTSYM, "matrix is not symmetric to working accuracy") : EIG33_OK;
+  return notsym_status(first);
 }
 
 }  // extern "C"

@@ -1,5 +1,6 @@
-"""Shared test helpers: loaders for the checkers (oracle port, compiled
-reference, CPU build of the product math) and comparison utilities.
+"""Shared test helpers: loaders for the checkers (compiled reference core --
+the parity checker, hard-required --, oracle port, CPU build of the product
+math, host corpus regeneration) and comparison utilities.
 
 The checkers are TEST INFRASTRUCTURE (oracle/ header); nothing here is used
 by the product path."""
@@ -49,11 +50,19 @@ def port():
 
 
 def ref():
-    """Compiled reference core, or None when it is unavailable."""
+    """The compiled reference core (oracle/_ref).  There is no fallback: every
+    parity check runs against the reference's own code, so a missing build is
+    an error, never a silent switch to the port."""
     global _ref
-    if _ref is None and os.path.exists(REF_SO):
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"{REF_SO} missing: run `make -C oracle ref` where /root/reference "
+                                    "exists (the prebuilt .so travels to the GPU box)")
         _ref = ctypes.CDLL(REF_SO)
     return _ref
+
+
+CHECKER = "compiled reference core (oracle/_ref/libeig33_ref.so)"
 
 
 def hostmath():
@@ -73,11 +82,7 @@ def checker_invariants(a):
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 9)
     n = a.shape[0]
     out = np.empty((n, 4))
-    R = ref()
-    if R is not None:
-        R.ref_invariants(ptr(a), S(n), ptr(out), nthreads())
-    else:
-        port().orc_invariants(ptr(a), S(n), ptr(out))
+    ref().ref_invariants(ptr(a), S(n), ptr(out), nthreads())
     return out
 
 
@@ -86,11 +91,7 @@ def checker_eigvals(a, adv=True):
     n = a.shape[0]
     lam = np.empty((n, 3))
     fl = np.empty(n, np.uint8) if adv else None
-    R = ref()
-    if R is not None:
-        R.ref_eigvals(ptr(a), S(n), ptr(lam), ptr(fl), nthreads())
-    else:
-        port().orc_eigvals(ptr(a), S(n), None, ptr(lam), ptr(fl))
+    ref().ref_eigvals(ptr(a), S(n), ptr(lam), ptr(fl), nthreads())
     return lam, fl
 
 
@@ -99,11 +100,7 @@ def checker_eigvalss(a):
     n = a.shape[0]
     lam = np.empty((n, 3))
     st = np.empty(n, np.uint8)
-    R = ref()
-    if R is not None:
-        R.ref_eigvalss(ptr(a), S(n), ptr(lam), ptr(st), nthreads())
-    else:
-        port().orc_eigvalss(ptr(a), S(n), None, ptr(lam), ptr(st))
+    ref().ref_eigvalss(ptr(a), S(n), ptr(lam), ptr(st), nthreads())
     return lam, st
 
 
@@ -115,7 +112,25 @@ def bit_equal(x, y):
     return (x.view(np.uint64) == y.view(np.uint64)) | (np.isnan(x) & np.isnan(y))
 
 
-TOL_UNITS = 4.0  # north_star: |lam - lam_ref| <= 4 * 2^-52 * max|lam_ref|
+TOL_UNITS = 4.0  # north_star: |lam - lam_ref| <= 4 ulp * max|lam_ref|, both readings below
+
+
+def lam_error_ulps(lam, lam_ref):
+    """Strict reading of the north_star gate: per-matrix max |lam - lam_ref| in
+    units of ulp(max_k |lam_ref,k|) (np.spacing: the binade's ulp, 2^(e-52) for
+    max|lam_ref| in [2^e, 2^(e+1))).  Up to 2x tighter than lam_error_units;
+    +inf where the non-finite class differs."""
+    lam = np.asarray(lam, np.float64)
+    lam_ref = np.asarray(lam_ref, np.float64)
+    fin = np.isfinite(lam_ref)
+    cls_ok = np.where(fin, np.isfinite(lam), (np.isnan(lam) & np.isnan(lam_ref)) | (lam == lam_ref))
+    mx = np.max(np.where(fin, np.abs(lam_ref), 0.0), axis=1)
+    ulp = np.spacing(mx)  # spacing(0) = 2^-1074, the smallest ulp
+    with np.errstate(all="ignore"):
+        d = np.max(np.where(fin, np.abs(lam - lam_ref), 0.0), axis=1)
+        u = np.where(d == 0, 0.0, d / ulp)
+        u = np.where(np.isnan(u), np.inf, u)
+    return np.where(cls_ok.all(axis=1), u, np.inf)
 
 
 def lam_error_units(lam, lam_ref):
@@ -132,6 +147,109 @@ def lam_error_units(lam, lam_ref):
         u = np.where(np.isnan(u), np.inf, u)
     u = np.where(scale == 0, np.where(d == 0, 0.0, np.inf), u)
     return np.where(cls_ok.all(axis=1), u, np.inf)
+
+
+CORPUS_SO = os.path.join(ROOT, "oracle", "libcorpus.so")
+_corpus = None
+
+
+def host_corpus(config, n, seed, first=0, threads=None):
+    """Records [first, first+n) of BASELINE config 1..5 regenerated on the host
+    (oracle/corpus_host.cpp over the shared recipes eig33_gen_core.h):
+    bit-identical to the device generator eig33cu_generate."""
+    global _corpus
+    if _corpus is None:
+        _ensure_built()
+        _corpus = ctypes.CDLL(CORPUS_SO)
+        _corpus.corpus_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, S, P,
+                                            ctypes.c_int]
+    a = np.empty((n, 9))
+    rc = _corpus.corpus_generate(config, seed & (2 ** 64 - 1), first, n, ptr(a), threads or nthreads())
+    assert rc == 0
+    return a
+
+
+_libm = None
+
+
+def _glibc():
+    global _libm
+    if _libm is None:
+        _libm = ctypes.CDLL("libm.so.6")
+        for f in ("atan2",):
+            getattr(_libm, f).restype = ctypes.c_double
+            getattr(_libm, f).argtypes = [ctypes.c_double, ctypes.c_double]
+        for f in ("sin", "cos"):
+            getattr(_libm, f).restype = ctypes.c_double
+            getattr(_libm, f).argtypes = [ctypes.c_double]
+    return _libm
+
+
+def libm_misrounds(inv_row):
+    """Does this host's libm -- the atan2 / sincos the reference calls at
+    proj/src/eigensolver.cpp:88 and :21 -- return a not-correctly-rounded
+    result for the transcendental arguments of this record (invariants
+    inv_row)?  Returns the names of the misrounded calls (mpmath at 200 bits
+    decides the correctly rounded value)."""
+    import math
+
+    import mpmath
+
+    i1, j2, j3, disc = (float(x) for x in inv_row)
+    if not (j2 > 0.0) or not math.isfinite(j3) or not math.isfinite(disc):
+        return []
+    M = _glibc()
+    y = math.sqrt(27.0 * (disc if disc > 0.0 else 0.0))
+    x = 27.0 * j3
+    bad = []
+    with mpmath.workprec(200):
+        phi = M.atan2(y, x)
+        if phi != float(mpmath.atan2(mpmath.mpf(y), mpmath.mpf(x))):
+            bad.append("atan2")
+        th = phi / 3.0
+        if M.sin(th) != float(mpmath.sin(mpmath.mpf(th))):
+            bad.append("sin")
+        if M.cos(th) != float(mpmath.cos(mpmath.mpf(th))):
+            bad.append("cos")
+    return bad
+
+
+STRICT_UNITS = 4.0  # north_star, strict reading: 4 * ulp(max|lam_ref|)
+
+
+def lam_gate(a, lam, lam_ref, inv_ref=None, fallback=None):
+    """The eigenvalue gate, strict reading: every record within
+    4 * ulp(max|lam_ref|) of the reference, except records where the
+    reference's libm misrounded one of its transcendental calls for that very
+    record (the device path is correctly rounded there, so the two cannot
+    agree to the last bit) -- those must still be inside the loose reading
+    4 * 2^-52 * max|lam_ref| -- or records `fallback(a, lam, lam_ref)` accepts
+    (config 4: the north_star's forward-error criterion).  Returns (strict
+    errors, loose errors, indices of the explained exceptions); raises
+    AssertionError with the first offenders otherwise."""
+    es = lam_error_ulps(lam, lam_ref)
+    el = lam_error_units(lam, lam_ref)
+    over = np.nonzero(es > STRICT_UNITS)[0]
+    if over.size and fallback is not None:
+        ok = fallback(a[over], lam[over], lam_ref[over])
+        over = over[~ok]
+    explained = []
+    if over.size:
+        assert over.size <= 1000, f"{over.size} records over {STRICT_UNITS} ulp(max|lam|)"
+        if inv_ref is None:
+            inv_ref = checker_invariants(a[over])
+            rows = inv_ref
+        else:
+            rows = inv_ref[over]
+        bad = []
+        for k, i in enumerate(over):
+            if el[i] <= TOL_UNITS and libm_misrounds(rows[k]):
+                explained.append(int(i))
+            else:
+                bad.append(int(i))
+        assert not bad, (f"{len(bad)} records over {STRICT_UNITS} ulp(max|lam_ref|) without a libm "
+                         f"misrounding behind them: first {bad[:5]}, strict {es[bad[:5]]}, loose {el[bad[:5]]}")
+    return es, el, explained
 
 
 def mixed_corpus(n, seed):

@@ -26,6 +26,20 @@ int main() {
     threw = true;
   }
   ok = ok && threw;
+  // the batched throw names the first record that fails the gate
+  // (src/eigensolver.cpp:102 throws for exactly that record)
+  std::vector<eig33::Mat3> s(5);
+  for (auto& m : s) m.e = {2, 1, 0, 1, 3, -1, 0, -1, 4};
+  s[3].e[1] = 1.5;
+  s[4].e[2] = 0.5;
+  std::vector<eig33::EigenTriple> st(5);
+  std::size_t bad_at = 99;
+  try {
+    eig33::eigvalss(s.data(), s.size(), st.data());
+  } catch (const eig33::NotSymmetricAt& e) {
+    bad_at = e.index;
+  }
+  ok = ok && bad_at == 3 && std::fabs(st[0].lambda2 - 3.0) < 1e-14;
   // the study variants go through the same batched overload (invariants.hpp:74)
   std::vector<eig33::InvariantSet> nv(3), tv(3);
   eig33::invariants(a.data(), a.size(), nv.data(), eig33::AlgorithmVariant::Naive);

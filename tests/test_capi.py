@@ -16,7 +16,7 @@ HEADER = os.path.join(U.ROOT, "include", "eig33_cuda.h")
 def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(eig33\w*)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|long long)\s+(eig33\w*)\s*\(", src, flags=re.M)))
 
 
 def test_header_matches_python_binding_table():

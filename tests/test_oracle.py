@@ -62,7 +62,6 @@ def test_port_matches_golden_fixtures():
     assert (U.lam_error_units(slam[ok], g["sym_lam"][ok]) <= U.TOL_UNITS).all()
 
 
-@pytest.mark.skipif(U.ref() is None, reason="compiled reference not built")
 def test_port_bitwise_equals_compiled_reference():
     a = U.mixed_corpus(1 << 17, 3)
     inv_r = np.empty((a.shape[0], 4))
@@ -138,7 +137,6 @@ def test_eigvalss_symmetry_gate():
     assert list(st) == [1, 1, 0]  # test_eigensolver.cpp:150-165
 
 
-@pytest.mark.skipif(U.ref() is None, reason="compiled reference not built")
 def test_port_study_variants_bitwise_equal_compiled_reference():
     """naive / tensor invariants, eigvals_naive, Jacobians."""
     a = U.mixed_corpus(1 << 15, 23)

@@ -45,7 +45,9 @@ def _run(a_host, *, inv=True, flags=True):
     return [None if x is None else x.cpu().numpy() for x in r]
 
 
-def _assert_parity(a, lam, inv, flags, name, max_units=U.TOL_UNITS, lam_tol_fallback=None):
+def _assert_parity(a, lam, inv, flags, name, max_units=None, lam_tol_fallback=None):
+    """Invariants and flags bitwise; lambda through U.lam_gate (strict reading,
+    4 ulp(max|lam_ref|), libm-misrounding exceptions inside the loose reading)."""
     inv_r = U.checker_invariants(a)
     bad = ~U.bit_equal(inv, inv_r).all(axis=1)
     assert not bad.any(), f"{name}: {bad.sum()} invariant rows differ, first {np.nonzero(bad)[0][:5]}"
@@ -53,13 +55,10 @@ def _assert_parity(a, lam, inv, flags, name, max_units=U.TOL_UNITS, lam_tol_fall
     if flags is not None:
         fb = (flags & eig.FLAG_ADVISORY) != adv_r
         assert not fb.any(), f"{name}: advisory differs on {fb.sum()} records"
-    err = U.lam_error_units(lam, lam_r)
-    over = err > max_units
-    if over.any() and lam_tol_fallback is not None:
-        over[over] = ~lam_tol_fallback(a[over], lam[over], lam_r[over])
-    assert not over.any(), (f"{name}: {over.sum()} records over {max_units} units; worst "
-                            f"{np.max(err):.3g} at {np.argmax(err)}")
-    return err
+    es, el, explained = U.lam_gate(a, lam, lam_r, inv_ref=inv_r, fallback=lam_tol_fallback)
+    if max_units is not None:
+        assert el.max() <= max_units, f"{name}: worst {el.max():.3g} units"
+    return el
 
 
 def test_golden_fixtures_on_device():
@@ -67,7 +66,7 @@ def test_golden_fixtures_on_device():
     lam, inv, flags = _run(g["a"])
     assert U.bit_equal(inv, g["inv"]).all()
     assert ((flags & 1) == g["adv"]).all()
-    assert (U.lam_error_units(lam, g["lam"]) <= U.TOL_UNITS).all()
+    U.lam_gate(g["a"], lam, g["lam"])
     _assert_parity(g["a"], lam, inv, flags, "golden")
 
 
@@ -144,17 +143,21 @@ def test_config3_full_size_every_record():
     inv_h = inv.cpu().numpy()
     del lam, inv, r
     step = 1 << 25  # compare in slices to bound host temporaries
-    worst = 0.0
+    worst = worst_strict = 0.0
     exact = 0
+    explained = 0
     for lo in range(0, n, step):
         sl = slice(lo, lo + step)
         inv_r = U.checker_invariants(a[sl])
         assert U.bit_equal(inv_h[sl], inv_r).all(), f"invariants differ in [{lo}, {lo + step})"
         lam_r, _ = U.checker_eigvals(a[sl], adv=False)
-        err = U.lam_error_units(lam_h[sl], lam_r)
-        worst = max(worst, float(err.max()))
-        exact += int((err == 0).sum())
+        es, el, ex = U.lam_gate(a[sl], lam_h[sl], lam_r, inv_ref=inv_r)
+        worst = max(worst, float(el.max()))
+        worst_strict = max(worst_strict, float(es.max()))
+        explained += len(ex)
+        exact += int((el == 0).sum())
     assert worst <= U.TOL_UNITS, worst
+    assert explained <= 64, explained
     assert exact / n > 0.998
 
 
@@ -214,7 +217,7 @@ def test_eigvalss_device_and_host():
     assert (r_s.flags.cpu().numpy() == 0).all()
     lam_r, st_r = U.checker_eigvalss(a_d.cpu().numpy())
     assert (st_r == 0).all()
-    assert (U.lam_error_units(r_s.lam.cpu().numpy(), lam_r) <= U.TOL_UNITS).all()
+    U.lam_gate(a_d.cpu().numpy(), r_s.lam.cpu().numpy(), lam_r)
     # symmetry gate (test_eigensolver.cpp:150-165) -> flag bit1 on device, ValueError on host
     bad = np.array([[1.0, 1.0, 0, 1.0 + 1e-8, 2, 0, 0, 0, 3], U.KAT_MATRICES["rotation"],
                     [1.0, 1.0, 0, 1.0 + 2.0 ** -52, 2, 0, 0, 0, 3]])
@@ -225,7 +228,7 @@ def test_eigvalss_device_and_host():
         eig.eigvalss(bad)
     lam_h = eig.eigvalss(bad[2:]).lam
     lam_c, _ = U.checker_eigvalss(bad[2:])
-    assert (U.lam_error_units(lam_h, lam_c) <= U.TOL_UNITS).all()
+    U.lam_gate(bad[2:], lam_h, lam_c)
 
 
 def test_host_entry_points_equal_device_entry_points():
@@ -278,25 +281,84 @@ def test_host_staged_path_all_outputs():
         eig.eigvalss(s_)
 
 
-def test_multi_gpu_entry_points_on_available_devices():
-    """eig33_multi_{eigvals,eigvalss,invariants} over every visible device give
-    the single-device bits; asking for more devices than exist is an error."""
+def _device_lists():
+    ng = torch.cuda.device_count() if torch.cuda.is_available() else 1
+    lists = [[0], [0, 0], [0, 0, 0, 0, 0]]  # repeated devices: threads take turns on one pipeline
+    if ng >= 2:
+        lists += [list(range(ng)), [ng - 1, 0]]
+    return lists
+
+
+@pytest.mark.parametrize("devices", _device_lists())
+def test_multi_gpu_entry_points_on_available_devices(devices):
+    """eig33_multi_eigvals_on over shard->device lists give the single-device
+    bits (pageable input large enough for the staged pipeline, so the shard
+    threads' host copies run concurrently through the shared copy pool); the
+    ngpu form over every visible device too; asking for more devices than
+    exist is an error."""
     ng = torch.cuda.device_count()
-    a = U.mixed_corpus((1 << 17) + 11, 61)
-    s_ = a.copy()
-    s_[:, [3, 6, 7]] = s_[:, [1, 2, 5]]
+    if ng < 2:
+        print(f"NOTE: only {ng} CUDA device visible -- shards run on repeated device lists; "
+              "the cross-device path needs a multi-GPU box")
+    a = U.mixed_corpus(len(devices) * (1 << 18) + 11, 61)  # >= 8 MB pageable per shard
     r1 = eig.eigvals(a, return_invariants=True, return_flags=True)
-    rm = eig.multi_eigvals(a, ng, return_invariants=True, return_flags=True)
+    rm = eig.multi_eigvals(a, devices=devices, return_invariants=True, return_flags=True)
     assert U.bit_equal(rm.lam, r1.lam).all() and U.bit_equal(rm.inv, r1.inv).all()
     assert (rm.flags == r1.flags).all()
+    rn = eig.multi_eigvals(a, ng, return_invariants=True, return_flags=True)
+    assert U.bit_equal(rn.lam, r1.lam).all() and (rn.flags == r1.flags).all()
     assert U.bit_equal(eig.multi_invariants(a, ng), r1.inv).all()
+    s_ = a.copy()
+    s_[:, [3, 6, 7]] = s_[:, [1, 2, 5]]
     assert U.bit_equal(eig.multi_eigvalss(s_, ng).lam, eig.eigvalss(s_).lam).all()
-    k = s_.shape[0] // 8 + 5  # a grid record (entries O(1)): now clearly asymmetric
-    s_[k, 1] += 1.0
-    with pytest.raises(ValueError):
-        eig.multi_eigvalss(s_, ng)
     with pytest.raises(ValueError):
         eig.multi_eigvals(a, ng + 1)
+    with pytest.raises(ValueError):
+        eig.multi_eigvals(a, devices=[0, ng])
+
+
+def test_not_symmetric_reports_first_record():
+    """The batched eigvalss names the first record failing the gate -- the one
+    a loop of scalar calls throws on (src/eigensolver.cpp:102) -- through the C
+    ABI (eig33cu_last_notsym_index), the error text and the multi-GPU driver."""
+    a = eig.generate(1, (1 << 20) + 3, seed=5).cpu().numpy()  # bitwise symmetric, pageable
+    L = eig.lib()
+    for k in (0, 77, (1 << 19) + 1, (1 << 20) + 2):
+        b = a.copy()
+        b[k, 1] += 0.25
+        b[min(k + 5, b.shape[0] - 1), 5] += 0.25  # a second, later offender
+        first = k
+        with pytest.raises(ValueError, match=f"record {first}"):
+            eig.eigvalss(b)
+        assert L.eig33cu_last_notsym_index() == first
+        with pytest.raises(ValueError, match=f"record {first}"):
+            eig.multi_eigvalss(b, 1)
+        assert L.eig33cu_last_notsym_index() == first
+    eig.eigvalss(a)
+    assert L.eig33cu_last_notsym_index() == -1
+
+
+def test_host_call_restores_current_device():
+    """eig33_*_host switch to the requested device and restore the caller's
+    current device on return (a rank that did set_device(k) keeps k)."""
+    ng = torch.cuda.device_count()
+    a = U.mixed_corpus(1000, 3)
+    for cur in range(ng):
+        torch.cuda.set_device(cur)
+        for target in range(ng):
+            eig.eigvals(a, device=target)
+            assert torch.cuda.current_device() == cur
+    torch.cuda.set_device(0)
+
+
+def test_error_return_leaves_no_pending_copies():
+    """A failing host call (device index out of range mid-batch for the
+    multi-driver) returns an error and leaves the library usable."""
+    a = U.mixed_corpus(1 << 18, 4)
+    with pytest.raises(ValueError):
+        eig.eigvals(a, device=torch.cuda.device_count())
+    r = eig.eigvals(a)
+    assert np.isfinite(r.lam[: 1 << 16]).any()
 
 
 def test_shard_invariance_bitwise():
@@ -309,6 +371,19 @@ def test_shard_invariance_bitwise():
         bounds = [2 * (k * n // (2 * g)) for k in range(g)] + [n]
         parts = [eig.eigvals(a_d[lo:hi]).lam for lo, hi in zip(bounds[:-1], bounds[1:])]
         assert torch.equal(torch.cat(parts).view(torch.int64), full.view(torch.int64))
+
+
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
+def test_device_generator_equals_host_regeneration(config):
+    """eig33cu_generate and the host regeneration (oracle/libcorpus.so, used by
+    bench.py's reference arm) share eig33_gen_core.h and must agree bitwise --
+    the reference arm times the reference on exactly the GPU arm's records."""
+    for seed, first, n in ((1000 + config, 0, 1 << 16), (0x251100292, (1 << 20) - 3000, 1 << 13),
+                           (7, (3 << 20) - 77, 1 << 12), (2 ** 64 - 1, 12345678901, 999)):
+        dev = eig.generate(config, n, seed=seed, first_index=first).cpu().numpy()
+        host = U.host_corpus(config, n, seed, first)
+        same = dev.view(np.uint64) == host.view(np.uint64)
+        assert same.all(), f"config {config} seed {seed} first {first}: {(~same.all(axis=1)).sum()} records differ"
 
 
 def test_generator_is_counter_based():
@@ -347,7 +422,7 @@ def test_study_variants_on_device():
     compiled reference: bit-exact except eigvals_naive's lambda (tolerance)."""
     a = U.mixed_corpus(1 << 18, 31)
     n = a.shape[0]
-    R = U.ref() or pytest.skip("compiled reference not available")
+    R = U.ref()
     for name, v in (("Naive", 1), ("NaiveTensor", 2)):
         got = eig.invariants(a, variant=name)
         want = np.empty((n, 4))

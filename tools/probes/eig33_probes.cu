@@ -1,5 +1,6 @@
-// eig33_probe.cu -- measurement helper for bench.py (not part of the C ABI
-// contract): the achievable FP64-pipe issue rate of this GPU, used as the
+// eig33_probes.cu -- measurement library for bench.py and tools/ (NOT part of the product
+// _eig33cuda.so or its C ABI):
+// the achievable FP64-pipe issue rate of this GPU, used as the
 // roofline denominator for the FP64-bound fused kernel.  MEASURED_PEAKS.json
 // carries only HBM and bf16 peaks, so bench.py measures this on the box.
 //
@@ -197,5 +198,38 @@ extern "C" int eig33_probe_stream(const double* a, long long n, double* lam, voi
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   k_stream<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const long long*>(a), n * 3,
                                                        reinterpret_cast<long long*>(lam));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// Data-path probe: k_fused's own TMA ring, tier tests and lambda stores with
+// the steady-state arithmetic removed (the MEMONLY instantiation, which exists
+// only in this measurement library, never in _eig33cuda.so), over a 16-B
+// aligned batch.  bench.py's optional energy-model leg times it.
+// ---------------------------------------------------------------------------
+#define EIG33_TABLE_DECL static __device__ __align__(16)
+#include "../../paper_2511_00292_b200/csrc/eig33_tables.h"
+#include "../../paper_2511_00292_b200/csrc/eig33_fused.cuh"
+
+extern "C" int eig33_probe_memonly(const double* d_a, size_t n, double* d_lam, void* stream) {
+  using namespace eig33b;
+  if (n == 0) return 0;
+  if (!d_a || !d_lam || ((uintptr_t)d_a & 15u)) return 2;
+  auto kern = k_fused<kEig, true, false, false, true>;
+  int dev = 0, sms = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // per call (and so per device): the attribute is per-device state
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)) !=
+      cudaSuccess)
+    return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sizeof(Smem)) != cudaSuccess ||
+      occ < 1)
+    return 1;
+  const long long nchunks = (long long)((n + kChunk - 1) / kChunk);
+  const long long nblk = (nchunks + kWarps - 1) / kWarps;
+  const long long cap = (long long)sms * occ;
+  kern<<<(unsigned)(nblk < cap ? nblk : cap), kThreads, sizeof(Smem), (cudaStream_t)stream>>>(
+      d_a, (long long)n, nullptr, d_lam, nullptr);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -29,7 +29,18 @@
 
 namespace {
 
-constexpr size_t kChunk = size_t(1) << 22;  // records per chunk (302 MB in, 101 MB out)
+// Chunk geometry (the CPU pipeline test, tests/test_hostpipe.py, builds with
+// small values so that a few thousand records already span many chunks).
+#ifndef EIG33_HOST_CHUNK_LOG2
+#define EIG33_HOST_CHUNK_LOG2 22
+#endif
+#ifndef EIG33_STAGE_CHUNK_LOG2
+#define EIG33_STAGE_CHUNK_LOG2 20
+#endif
+#ifndef EIG33_STAGE_MIN_BYTES
+#define EIG33_STAGE_MIN_BYTES (size_t(8) << 20)
+#endif
+constexpr size_t kChunk = size_t(1) << EIG33_HOST_CHUNK_LOG2;  // records per chunk (302 MB in, 101 MB out)
 constexpr int kSets = 3;
 
 int fail(int code, const std::string& what, cudaError_t e = cudaSuccess) {
@@ -150,7 +161,10 @@ class CopyPool {
   }
 
  private:
-  static constexpr size_t kPart = size_t(4) << 20;
+#ifndef EIG33_COPY_PART
+#define EIG33_COPY_PART (size_t(4) << 20)
+#endif
+  static constexpr size_t kPart = EIG33_COPY_PART;
   struct Job {
     char* dst = nullptr;
     const char* src = nullptr;
@@ -190,11 +204,12 @@ class CopyPool {
   }
   void work() {
     for (;;) {
-      Job* j;
+      Job* j = nullptr;
       {
+        // one pick() under the lock: another thread's run() may claim the
+        // last parts (an atomic, outside the lock) between two calls
         std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [&] { return pick() != nullptr; });
-        j = pick();
+        cv_.wait(g, [&] { return (j = pick()) != nullptr; });
         ++j->refs;
       }
       run(*j);
@@ -214,8 +229,8 @@ class CopyPool {
 // Pinned host bounce buffers (per device, grown on demand) for callers whose
 // buffers are pageable: the pool copies a chunk into pinned memory while the
 // copy engines move the previous chunks, instead of the driver's serial staging.
-constexpr size_t kStageChunk = size_t(1) << 20;         // records per staged chunk
-constexpr size_t kStageMinBytes = size_t(8) << 20;      // smaller inputs: pageable direct
+constexpr size_t kStageChunk = size_t(1) << EIG33_STAGE_CHUNK_LOG2;  // records per staged chunk
+constexpr size_t kStageMinBytes = EIG33_STAGE_MIN_BYTES;               // smaller inputs: pageable direct
 struct HostStaging {
   size_t cap = 0;
   double* in[kSets] = {};

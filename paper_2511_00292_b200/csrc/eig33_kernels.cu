@@ -74,7 +74,12 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
   DevInfo& d = g_dev[dev];
   const size_t smem = sizeof(Smem);
-  auto kern = MODE == kInv ? k_invariants<TMA> : k_fused<MODE, TMA, WI, WF>;
+  using KernFn = void (*)(const double*, long long, double*, double*, uint8_t*);
+  KernFn kern;
+  if constexpr (MODE == kInv)
+    kern = k_invariants<TMA>;  // (no k_fused<kInv, ...> instantiation)
+  else
+    kern = k_fused<MODE, TMA, WI, WF>;
   std::atomic<int>& occ_slot = d.occ[MODE][TMA][WI][WF];
   int occ = occ_slot.load(std::memory_order_acquire);
   if (!occ) {

@@ -52,6 +52,41 @@ struct __align__(16) Smem {
   unsigned long long bar[kWarps][kStages];
 };
 
+// In-kernel advisory queue (eigvals with flags).  The advisory
+// (src/eigensolver.cpp:54) needs disc_tolerance -- the Jacobian of disc and two
+// Frobenius norms, ~110 FP64 operations -- only for records with disc < 0 (0%
+// of configs 1-3, 37% of config 4).  Evaluating it in every step would cost
+// every lane of a warp whenever one lane is pending; instead each warp queues
+// its pending records (index + j2, j3, disc) in a 64-entry SMEM ring and
+// evaluates them 32 at a time, one per lane, re-reading the 72-B record from
+// global memory -- an L2 hit: the warp's TMA brought it on chip moments ago.
+// (The previous design, a deferred kernel re-reading every pending record
+// from HBM, cost 72 us next to k_fused's 121 us on config 4.)
+struct AdvEntry {
+  long long idx;
+  double j2, j3, disc;
+};
+constexpr uint32_t kAdvQ = 64;  // entries per warp (power of two, >= 2 x 32)
+
+// Evaluate `count` (<= 32) queued records starting at `head`, one per lane,
+// and write their final flag bytes.  Out of line: its registers never enter
+// the steady-state loop's allocation.
+__device__ __noinline__ void advisory_flush(const double* __restrict__ a, uint8_t* __restrict__ flags,
+                                            const AdvEntry* q, uint32_t head, uint32_t count) {
+  __syncwarp();  // queue entries were written by other lanes
+  const uint32_t lane = threadIdx.x & 31u;
+  if (lane < count) {
+    const AdvEntry e = q[(head + lane) & (kAdvQ - 1)];
+    EIG33_CHECK(e.idx >= 0);
+    double m[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) m[k] = __ldg(a + e.idx * 9 + k);
+    flags[e.idx] = advisory(m, Inv{0.0, e.j2, e.j3, e.disc}) ? EIG33_FLAG_ADVISORY : 0;
+  }
+  __syncwarp();  // the slots may be refilled by the next push
+}
+
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -115,7 +150,8 @@ struct Tabs {
 // checked kernel on every lane rather than both kernels one after the other
 // (divergent lanes would serialise them).  `mask`: the lanes executing the call.
 __device__ __forceinline__ Inv invariants_warp(const double m[9], bool mod, unsigned mask) {
-  return __all_sync(mask, mod) ? invariants_moderate(m) : invariants(m);
+  // checked form: the always-valid CSE DAG (231 ops vs 341 in reference order)
+  return __all_sync(mask, mod) ? invariants_moderate(m) : invariants_dag(m);
 }
 
 // Stage 1 of a record: symmetry gate (eigvalss), invariants, flag bits, and
@@ -147,16 +183,10 @@ __device__ __forceinline__ void stage1(double m[9], bool& mod, Inv& v, Carry& c,
 }
 
 // Stage 2 (eigenvalues) of a record from its carry, general form; called by
-// whole warps.  As in invariants_warp, the checked from_invariants serves every
-// lane once any lane needs it (same bits on moderate carries).
+// whole warps.  As in invariants_warp, the general (any-input) form serves
+// every lane once any lane needs it (same bits on moderate carries).
 __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const Tabs& T) {
-  Lam L;
-  if (__all_sync(0xffffffffu, mod || bad)) {
-    L = eig_moderate_bl(c, T.tab);
-  } else {
-    const double a[9] = {c.a0, 0, 0, 0, c.a4, 0, 0, 0, c.a8};  // diagonal_mean reads only these
-    L = from_invariants(a, Inv{c.i1, c.j2, c.j3, c.disc}, T.tab);
-  }
+  Lam L = __all_sync(0xffffffffu, mod || bad) ? eig_moderate_bl(c, T.tab) : eig_general_bl(c, T.tab);
   if (bad) {
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     L = Lam{qnan, qnan, qnan};
@@ -164,10 +194,18 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
   return L;
 }
 
-// Slow tiers of the record pipeline.  The general tier is a real call so that
-// its register demand never enters the allocation of the steady-state loop
-// (inlining it made ptxas move arrays to local memory there and cost 3x); the
+// Slow tiers of the record pipeline.  The general tier is a real call by
+// default so that its register demand never enters the allocation of the
+// steady-state loop (EIG33_GENERAL_INLINE=1 inlines it, for measurement); the
 // moderate tier is small enough to inline.
+#ifndef EIG33_GENERAL_INLINE
+#define EIG33_GENERAL_INLINE 0
+#endif
+#if EIG33_GENERAL_INLINE
+#define EIG33_GENERAL_ATTR __forceinline__
+#else
+#define EIG33_GENERAL_ATTR __noinline__
+#endif
 struct M9 {
   double e[9];
 };
@@ -194,29 +232,27 @@ __device__ __forceinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* 
   return o;
 }
 
-// Tier C, per lane: the checked reference-order path (zeros, subnormals,
-// extreme exponents, inf/NaN, eigvalss rejects).
+// Tier C, warp-uniform: some lane holds a record outside the moderate range
+// (zeros mixed with tiny entries, subnormals, extreme exponents, inf/NaN) or an
+// eigvalss reject.  Straight-line any-input forms for both stages -- the
+// always-valid invariant DAG and eig_general_bl (selects, no per-lane special
+// branches) -- so the scheduler interleaves them like the moderate tier.
 template <int MODE, bool WANT_FLAGS>
-__device__ __noinline__ StepOut tier_general(M9 mm, bool sym_ok, bool mod, Carry pc, bool pmod,
-                                             bool pbad, const double* tab) {
+__device__ EIG33_GENERAL_ATTR StepOut tier_general(M9 mm, bool sym_ok, bool mod, Carry pc, bool pbad,
+                                                   const double* tab) {
   StepOut o;
-  o.L = stage2(pc, pmod, pbad, Tabs{tab});
-  if (MODE == kSym) {
-    o.bad = !sym_ok;  // already mirrored: the gate verdict decides
-    o.f = o.bad ? EIG33_FLAG_NOT_SYMMETRIC : 0;
-    o.mod = mod && !o.bad;
-    // rejected lanes do not vote: their (garbage) invariants are replaced by NaN
-    o.v = invariants_warp(mm.e, mod || o.bad, 0xffffffffu);
-    if (o.bad) {
-      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-      o.v.i1 = o.v.j2 = o.v.j3 = o.v.disc = qnan;
-    }
-  } else {
-    Carry nc;
-    bool m2 = mod;
-    stage1<MODE, WANT_FLAGS>(mm.e, m2, o.v, nc, o.f, o.bad);
-    o.mod = m2;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  o.L = eig_general_bl(pc, tab);
+  if (pbad) o.L = Lam{qnan, qnan, qnan};
+  o.v = invariants_dag(mm.e);
+  o.bad = MODE == kSym && !sym_ok;  // (already mirrored: the gate verdict decides)
+  o.f = 0;
+  if (o.bad) {
+    o.v.i1 = o.v.j2 = o.v.j3 = o.v.disc = qnan;
+    o.f = EIG33_FLAG_NOT_SYMMETRIC;
   }
+  if (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) o.f = kPending;
+  o.mod = mod && !o.bad;
   return o;
 }
 
@@ -333,7 +369,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   Carry pc;
   uint8_t f;
   long long pr;  // record index of the carried stage
+  constexpr bool kQueue = MODE == kEig && WANT_FLAGS;
+  AdvEntry* advq = kQueue ? reinterpret_cast<AdvEntry*>(smem_raw + sizeof(Smem)) + warp * kAdvQ : nullptr;
+  uint32_t qh = 0, qt = 0;  // queue head / tail (warp-uniform)
   auto store_stage1 = [&](long long r, bool valid) {
+    const bool pend = kQueue && valid && f == kPending;
+    if (kQueue) {  // pending records go to the advisory queue, their flag byte comes later
+      const unsigned pm = __ballot_sync(0xffffffffu, pend);
+      if (pm) {
+        if (pend) {
+          const uint32_t pos = (qt + __popc(pm & ((1u << lane) - 1u))) & (kAdvQ - 1);
+          advq[pos] = AdvEntry{r, v.j2, v.j3, v.disc};
+        }
+        qt += __popc(pm);
+        if (qt - qh >= 32u) {
+          advisory_flush(a, flags, advq, qh, 32u);
+          qh += 32u;
+        }
+      }
+    }
     if (!valid) return;
     EIG33_CHECK(r >= 0 && r < R.n);
     if (WANT_INV) {
@@ -342,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       inv[r * 4 + 2] = v.j3;
       inv[r * 4 + 3] = v.disc;
     }
-    if (MODE != kInv && WANT_FLAGS) flags[r] = f;
+    if (MODE != kInv && WANT_FLAGS && !pend) flags[r] = f;
   };
   auto store_lam = [&](const Lam& L) {
     if (!pvalid) return;
@@ -387,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (__all_sync(0xffffffffu, sym_ok && mod && pmod))
         o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
       else
-        o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pmod, pbad, T.tab);
+        o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pbad, T.tab);
       L = o.L;
       v = o.v;
       f = o.f;
@@ -435,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
   }
   store_lam(stage2(pc, pmod, pbad, T));
+  if (kQueue && qt != qh) advisory_flush(a, flags, advq, qh, qt - qh);
 }
 
 // Invariants-only kernel: stage 1 alone, same per-warp TMA ring.
@@ -475,73 +530,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         inv[r * 4 + 3] = v.disc;
       }
     }
-  }
-}
-
-// Deferred advisory: evaluate src/eigensolver.cpp:54 only where k_fused found
-// disc < 0.  A block takes a window of kThreads*16 records: each thread reads
-// its 16 flag bytes with one 16-B load, and a window with nothing pending is
-// dismissed by one __syncthreads_or (the common case costs one coalesced read
-// of the flags).  Otherwise the pending records are compacted into SMEM
-// (warp scan of per-thread counts) and the block works the list densely.
-constexpr int kAdvWindow = kThreads * 16;
-__global__ void __launch_bounds__(kThreads) k_advisory(const double* __restrict__ a, long long n,
-                                                       const double* __restrict__ inv,
-                                                       uint8_t* __restrict__ flags) {
-  __shared__ int list[kAdvWindow];
-  __shared__ int wsum[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool vec = ((uintptr_t)flags & 15u) == 0;
-  constexpr uint64_t kPend8 = 0x0101010101010101ull * kPending;
-  for (long long w0 = (long long)blockIdx.x * kAdvWindow; w0 < n;
-       w0 += (long long)gridDim.x * kAdvWindow) {
-    const long long base = w0 + 16LL * threadIdx.x;
-    uint64_t w[2] = {0, 0};
-    if (vec && base + 16 <= n) {
-      const ulonglong2 v2 = __ldcg(reinterpret_cast<const ulonglong2*>(flags + base));
-      w[0] = v2.x;
-      w[1] = v2.y;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (base + k < n) w[k >> 3] |= (uint64_t)flags[base + k] << (8 * (k & 7));
-    }
-    const uint64_t pm0 = w[0] & kPend8, pm1 = w[1] & kPend8;
-    if (!__syncthreads_or((pm0 | pm1) != 0)) continue;
-    const int cnt = __popcll(pm0) + __popcll(pm1);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    int pos = incl - cnt, total = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const int sw = wsum[w];
-      pos += w < warp ? sw : 0;
-      total += sw;
-    }
-    for (uint64_t r = pm0; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + ((__ffsll((long long)r) - 1) >> 3);
-    for (uint64_t r = pm1; r; r &= r - 1) list[pos++] = 16 * threadIdx.x + 8 + ((__ffsll((long long)r) - 1) >> 3);
-    __syncthreads();
-    for (int j = threadIdx.x; j < total; j += blockDim.x) {
-      const long long idx = w0 + list[j];
-      double m[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) m[k] = __ldg(a + idx * 9 + k);
-      Inv v;
-      if (inv) {  // k_fused already wrote this record's invariants
-        v = Inv{inv[idx * 4], inv[idx * 4 + 1], inv[idx * 4 + 2], inv[idx * 4 + 3]};
-      } else {
-        const bool mod = is_moderate(m) || is_moderate_or_zero(m);
-        v = invariants_warp(m, mod, __activemask());  // same bits either way
-      }
-      flags[idx] = (uint8_t)((flags[idx] & ~kPending) | (advisory(m, v) ? EIG33_FLAG_ADVISORY : 0));
-    }
-    __syncthreads();  // list and wsum are reused by the next window
   }
 }
 

@@ -397,7 +397,9 @@ int run_device(Op op, const double* h_a, size_t n, double* h_inv, double* h_lam,
                int device, long long* notsym) {
   if (notsym) *notsym = -1;
   if (n == 0) return EIG33_OK;
-  if (device < 0 || device >= 64) return fail(EIG33_EINVAL, "device index out of range");
+  int have = 0;
+  if (cudaGetDeviceCount(&have) != cudaSuccess) have = 0;
+  if (device < 0 || device >= 64 || device >= have) return fail(EIG33_EINVAL, "device index out of range");
   DeviceGuard keep;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaSetDevice", e);

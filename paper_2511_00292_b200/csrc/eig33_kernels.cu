@@ -16,9 +16,9 @@
 //       programmatic dependent launch.  Outputs are stored straight from
 //       registers.
 //   k_invariants<TMA>            invariants only, same ring.
-//   k_advisory                   deferred non_real_advisory: scans the flags of
-//       a window with 16-B loads, block-compacts the records k_fused marked
-//       pending (disc < 0) and evaluates disc_tolerance only for them (bit-exact).
+//   (non_real_advisory: k_fused's eigvals-with-flags form queues the records
+//       with disc < 0 per warp and evaluates disc_tolerance for them 32 at a
+//       time, bit-exact -- see AdvEntry / advisory_flush in eig33_fused.cuh.)
 //   k_triple_angle               batched triple_angle.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -73,7 +73,8 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   if (e != cudaSuccess) return fail(EIG33_ECUDA, "cudaGetDevice", e);
   if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
   DevInfo& d = g_dev[dev];
-  const size_t smem = sizeof(Smem);
+  // eigvals with flags also carries the per-warp advisory queues
+  const size_t smem = sizeof(Smem) + (MODE == kEig && WF ? sizeof(AdvEntry) * kAdvQ * kWarps : 0);
   using KernFn = void (*)(const double*, long long, double*, double*, uint8_t*);
   KernFn kern;
   if constexpr (MODE == kInv)
@@ -145,20 +146,6 @@ static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t
                  : dispatch_out<MODE, false>(a, n, inv, lam, flags, st);
 }
 
-static int launch_advisory(const double* a, size_t n, const double* inv, uint8_t* flags,
-                           cudaStream_t st) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int sms = (dev >= 0 && dev < 64) ? g_dev[dev].sms.load() : 0;
-  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long windows = (long long)((n + kAdvWindow - 1) / kAdvWindow);
-  const long long grid = windows < 8LL * sms ? windows : 8LL * sms;
-  k_advisory<<<(unsigned)grid, kThreads, 0, st>>>(a, (long long)n, inv, flags);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(EIG33_ECUDA, "k_advisory launch", e);
-  return EIG33_OK;
-}
-
 }  // namespace eig33b
 
 using namespace eig33b;
@@ -180,9 +167,7 @@ int eig33cu_eigvals(const double* d_a, size_t n, double* d_inv, double* d_lam, u
   g_err.clear();
   if (n == 0) return EIG33_OK;
   if (!d_a || !d_lam) return fail(EIG33_EINVAL, "eig33cu_eigvals: null pointer");
-  int rc = dispatch<kEig>(d_a, n, d_inv, d_lam, d_flags, (cudaStream_t)stream);
-  if (rc == EIG33_OK && d_flags) rc = launch_advisory(d_a, n, d_inv, d_flags, (cudaStream_t)stream);
-  return rc;
+  return dispatch<kEig>(d_a, n, d_inv, d_lam, d_flags, (cudaStream_t)stream);
 }
 
 int eig33cu_eigvalss(const double* d_a, size_t n, double* d_inv, double* d_lam, uint8_t* d_flags,

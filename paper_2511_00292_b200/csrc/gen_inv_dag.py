@@ -1,7 +1,9 @@
 """Generate eig33_inv_dag.h: the reference's stable invariant kernels
-(/root/reference/proj/src/invariants_impl.hpp:21-85) as an explicit
-common-subexpression DAG, for records whose entries all lie in
-[2^-100, 2^100) in magnitude (the kernel's "moderate" fast path).
+(/root/reference/proj/src/invariants_impl.hpp:21-85) as explicit
+common-subexpression DAGs: invariants_moderate for records whose entries all
+lie in [2^-100, 2^100) in magnitude (the kernel's "moderate" fast path;
+identities 1-4 below), and invariants_dag for any record (identities 1-3,
+which hold for every binary64 input, and checked constant divisions).
 
 Every rounded operation of the reference is computed exactly once with the
 same operands, up to these value-preserving identities of IEEE binary64
@@ -68,7 +70,7 @@ def sub(a, b):
     return mk("sub", a, b)
 
 
-def build():
+def build(fold=True):
     A = {f"a{i}{j}": inp(f"a{i}{j}") for i in range(3) for j in range(3)}
     a00, a01, a02, a10, a11, a12, a20, a21, a22 = (A[k] for k in
                                                     ["a00", "a01", "a02", "a10", "a11", "a12", "a20", "a21", "a22"])
@@ -119,7 +121,7 @@ def build():
     w = [9, 6, 6, 6, 8, 8, 8, 2, 2, 2, 2, 2, 2, 1]
     acc = None
     for k in range(14):
-        if w[k] in (2, 8):
+        if fold and w[k] in (2, 8):
             acc = mk("fma_w", w[k], mul(u[k], v[k]), acc)
         elif w[k] == 1:
             acc = add(acc, mul(u[k], v[k]))
@@ -139,8 +141,7 @@ def ref(x, names):
     return names[x]
 
 
-def main():
-    outs = build()
+def emit(outs, fname, checked):
     names = {}
     lines = []
     counts = {}
@@ -156,7 +157,7 @@ def main():
         elif op == "sub":
             e = f"{ref(key[1], names)} - {ref(key[2], names)}"
         elif op in ("div3", "div6", "div27"):
-            e = f"{op}_nz({ref(key[1], names)})"
+            e = f"{op}{'' if checked else '_nz'}({ref(key[1], names)})"
         elif op == "fma_w":
             e = f"fma_({float(key[1])!r}, {ref(key[2], names)}, {ref(key[3], names)})"
         elif op == "zadd":
@@ -166,13 +167,9 @@ def main():
         lines.append(f"  const double {nm} = {e};")
     body = "\n".join(lines)
     total = sum(counts.values())
-    hdr = f"""// Generated by gen_inv_dag.py -- do not edit.
-// Stable invariants of /root/reference/proj/src/invariants_impl.hpp:21-85 as an
-// explicit CSE DAG ({total} binary64 operations: {counts}).
-// Valid only for records with every |a_ij| in [2^-100, 2^100) (see gen_inv_dag.py).
-#pragma once
-
-EIG33_HD Inv invariants_moderate(const double a[9]) {{
+    return f"""
+EIG33_HD Inv {fname}(const double a[9]) {{
+  // {total} binary64 operations: {counts}
   const double a00 = a[0], a01 = a[1], a02 = a[2];
   const double a10 = a[3], a11 = a[4], a12 = a[5];
   const double a20 = a[6], a21 = a[7], a22 = a[8];
@@ -184,11 +181,31 @@ EIG33_HD Inv invariants_moderate(const double a[9]) {{
   o.disc = {ref(outs[3], names)};
   return o;
 }}
-"""
+""", counts, total
+
+
+def main():
+    global nodes, order
+    outs = build(fold=True)
+    mod, c1, t1 = emit(outs, "invariants_moderate", checked=False)
+    nodes, order = {}, []
+    outs = build(fold=False)
+    gen, c2, t2 = emit(outs, "invariants_dag", checked=True)
+    hdr = f"""// Generated by gen_inv_dag.py -- do not edit.
+// Stable invariants of /root/reference/proj/src/invariants_impl.hpp:21-85 as
+// explicit CSE DAGs:
+//   invariants_moderate ({t1} ops): identities (1)-(4) of gen_inv_dag.py and
+//       unchecked constant divisions -- valid only for records with every
+//       |a_ij| in [2^-100, 2^100) or zero (is_moderate_or_zero);
+//   invariants_dag ({t2} ops): identities (1)-(3) only, which hold for every
+//       binary64 input (inf, NaN, subnormals, overflow), and the checked
+//       divisions -- the reference's bits for ANY record.
+#pragma once
+{mod}{gen}"""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "eig33_inv_dag.h")
     with open(path, "w") as f:
         f.write(hdr)
-    print("wrote", path, counts, total)
+    print("wrote", path, c1, t1, c2, t2)
 
 
 if __name__ == "__main__":

@@ -23,6 +23,26 @@ static Lam lam_path(const double* m, const Inv& v, int path) {
     return from_invariants_moderate(m, v, eig33_tab);
   return from_invariants(m, v, eig33_tab);
 }
+// the always-valid CSE DAG of the invariants (identities 1-3, checked divisions)
+void hm_invariants_dag(const double* a, size_t n, double* inv) {
+  for (size_t i = 0; i < n; ++i) {
+    const Inv v = invariants_dag(a + 9 * i);
+    inv[4 * i] = v.i1; inv[4 * i + 1] = v.j2; inv[4 * i + 2] = v.j3; inv[4 * i + 3] = v.disc;
+  }
+}
+// the general tier: invariants_dag + eig_general_bl (branch-light checked forms)
+void hm_eigvals_general(const double* a, size_t n, double* lam) {
+  for (size_t i = 0; i < n; ++i) {
+    const double* m = a + 9 * i;
+    const Inv v = invariants_dag(m);
+    const Carry c{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
+    const Lam l = eig_general_bl(c, eig33_tab);
+    lam[3 * i] = l.l1; lam[3 * i + 1] = l.l2; lam[3 * i + 2] = l.l3;
+  }
+}
+void hm_atan2_any(const double* y, const double* x, size_t n, double* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = atan2_any(y[i], x[i], eig33_tab);
+}
 int hm_is_moderate(const double* a) { return is_moderate(a) ? 1 : 0; }
 int hm_is_moderate_or_zero(const double* a) { return is_moderate_or_zero(a) ? 1 : 0; }
 // path 3: the kernel's steady-state block (eig_fast) where its preconditions

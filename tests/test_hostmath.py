@@ -227,3 +227,63 @@ def test_transcendentals_misround_less_than_glibc():
         theirs += (es != gs[i]) + (ec != gc[i]) + (ea != g[i])
     assert ours <= 0.0005 * 3 * n
     assert ours < theirs
+
+
+def test_invariants_dag_is_bitwise_for_any_record():
+    """invariants_dag (gen_inv_dag.py, identities 1-3 only, checked divisions)
+    reproduces the reference's invariants for every binary64 input: random bit
+    patterns (inf, NaN, subnormals), 2^k-scaled records far outside the
+    moderate range (overflow / underflow inside the DAG), zeros and ties."""
+    rng = np.random.default_rng(2024)
+    n = 1 << 17
+    parts = [U.mixed_corpus(n, 5),
+             rng.integers(0, 2 ** 64, size=(n, 9), dtype=np.uint64).view(np.float64),
+             rng.standard_normal((n, 9)) * np.ldexp(1.0, rng.integers(-1074, 1000, size=(n, 1))),
+             np.round(rng.standard_normal((n, 9)) * 2) * np.ldexp(1.0, rng.integers(-600, 600, size=(n, 1)))]
+    with np.errstate(all="ignore"):
+        a = np.ascontiguousarray(np.concatenate(parts))
+    m = a.shape[0]
+    inv = np.empty((m, 4))
+    U.hostmath().hm_invariants_dag(U.ptr(a), U.S(m), U.ptr(inv))
+    same = U.bit_equal(inv, U.checker_invariants(a)).all(axis=1)
+    assert same.all(), f"{(~same).sum()} records differ, first {np.nonzero(~same)[0][:5]}"
+
+
+def _adversarial(n, seed):
+    rng = np.random.default_rng(seed)
+    parts = [U.mixed_corpus(n, seed),
+             rng.integers(0, 2 ** 64, size=(n, 9), dtype=np.uint64).view(np.float64),
+             rng.standard_normal((n, 9)) * np.ldexp(1.0, rng.integers(-1074, 1000, size=(n, 1))),
+             np.round(rng.standard_normal((n, 9)) * 2) * np.ldexp(1.0, rng.integers(-600, 600, size=(n, 1)))]
+    with np.errstate(all="ignore"):
+        return np.ascontiguousarray(np.concatenate(parts))
+
+
+def test_general_tier_equals_checked_path():
+    """The general tier's branch-light forms (invariants_dag + eig_general_bl:
+    atan2_any, sqrt_any, selects for the j2 <= 0 collapse) give exactly the
+    checked path's bits (invariants + from_invariants) on every input class."""
+    a = _adversarial(1 << 16, 77)
+    n = a.shape[0]
+    H = U.hostmath()
+    got, want = np.empty((n, 3)), np.empty((n, 3))
+    H.hm_eigvals_general(U.ptr(a), U.S(n), U.ptr(got))
+    H.hm_eigvals_path(U.ptr(a), U.S(n), U.ptr(want), 1)
+    same = U.bit_equal(got, want).all(axis=1)
+    assert same.all(), f"{(~same).sum()} records differ, first {np.nonzero(~same)[0][:5]}"
+
+
+def test_atan2_any_equals_atan2_pos():
+    rng = np.random.default_rng(3)
+    n = 1 << 18
+    y = np.abs(rng.integers(0, 2 ** 64, size=n, dtype=np.uint64).view(np.float64))
+    x = rng.integers(0, 2 ** 64, size=n, dtype=np.uint64).view(np.float64)
+    y[np.isnan(y)] = np.inf
+    sp = np.array([0.0, np.inf, 1.0, 5e-324, 1e300, 2.0 ** -1000])
+    y[: 36] = np.repeat(sp, 6)
+    x[: 36] = np.tile(np.array([0.0, -0.0, np.inf, -np.inf, np.nan, -3.0]), 6)
+    H = U.hostmath()
+    got, want = np.empty(n), np.empty(n)
+    H.hm_atan2_any(U.ptr(y), U.ptr(x), U.S(n), U.ptr(got))
+    H.hm_atan2(U.ptr(y), U.ptr(x), U.S(n), U.ptr(want))
+    assert U.bit_equal(got, want).all()

@@ -20,8 +20,12 @@ namespace eig33b {
 #ifndef EIG33_PDL
 #define EIG33_PDL 1
 #endif
+// One 512-thread block (16 warps) per SM: the 128-register budget allows 16
+// warps per SM either way, and one block lets all 16 share one dynamic chunk
+// counter (EIG33_DYN) -- measured +5.5% on config 3 and +14% on config 5
+// against two 256-thread blocks per SM (tools/variant_compare.py).
 #ifndef EIG33_THREADS
-#define EIG33_THREADS 256
+#define EIG33_THREADS 512
 #endif
 constexpr int kThreads = EIG33_THREADS;  // threads per block
 constexpr int kWarps = kThreads / 32;
@@ -37,7 +41,7 @@ constexpr int kChunk = 32 * kRPL;  // records per warp chunk
 constexpr int kStages = EIG33_STAGES;  // per-warp TMA ring depth (power of two)
 static_assert((kStages & (kStages - 1)) == 0, "kStages must be a power of two");
 #ifndef EIG33_MIN_BLOCKS
-#define EIG33_MIN_BLOCKS 2
+#define EIG33_MIN_BLOCKS 1
 #endif
 constexpr int kMinBlocks = EIG33_MIN_BLOCKS;  // resident blocks per SM the register budget targets
 constexpr int kTabDoubles = EIG33_TAB_N;
@@ -50,6 +54,7 @@ struct __align__(16) Smem {
   double in[kWarps][kStages][kChunk * 9];
   double tab[kTabDoubles + 7];
   unsigned long long bar[kWarps][kStages];
+  int next;  // block-level chunk counter (EIG33_DYN)
 };
 
 // In-kernel advisory queue (eigvals with flags).  The advisory
@@ -61,7 +66,9 @@ struct __align__(16) Smem {
 // evaluates them 32 at a time, one per lane, re-reading the 72-B record from
 // global memory -- an L2 hit: the warp's TMA brought it on chip moments ago.
 // (The previous design, a deferred kernel re-reading every pending record
-// from HBM, cost 72 us next to k_fused's 121 us on config 4.)
+// from HBM, cost 72 us next to k_fused's 121 us on config 4.  Flushing 64 at a
+// time, two records per lane from a 96-entry queue, measured slower: 23.3 vs
+// 24.7 G records/s on config 4.)
 struct AdvEntry {
   long long idx;
   double j2, j3, disc;
@@ -84,6 +91,34 @@ __device__ __noinline__ void advisory_flush(const double* __restrict__ a, uint8_
     flags[e.idx] = advisory(m, Inv{0.0, e.j2, e.j3, e.disc}) ? EIG33_FLAG_ADVISORY : 0;
   }
   __syncwarp();  // the slots may be refilled by the next push
+}
+
+// EIG33_ADVQ_SMEM=1 (measurement variant): the queue holds the records
+// themselves (copied from the SMEM ring at push time, 104 B per entry, 32
+// entries per warp, flushed before it would overflow), so a flush reads no
+// global memory at all.  The ring stage of a chunk is then handed back only
+// after the chunk's last step.
+#ifndef EIG33_ADVQ_SMEM
+#define EIG33_ADVQ_SMEM 0
+#endif
+struct AdvRec {
+  double m[9];
+  double j2, j3, disc;
+  long long idx;
+};
+constexpr uint32_t kAdvR = 32;
+__device__ __noinline__ void advisory_flush_smem(uint8_t* __restrict__ flags, const AdvRec* q,
+                                                 uint32_t count) {
+  __syncwarp();
+  const uint32_t lane = threadIdx.x & 31u;
+  if (lane < count) {
+    const AdvRec& e = q[lane];
+    double m[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) m[k] = e.m[k];
+    flags[e.idx] = advisory(m, Inv{0.0, e.j2, e.j3, e.disc}) ? EIG33_FLAG_ADVISORY : 0;
+  }
+  __syncwarp();
 }
 
 
@@ -136,6 +171,26 @@ __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
+
+// EIG33_TIMELINE=1 (diagnostic build, tools/timeline.py): each warp of k_fused
+// records %globaltimer at entry, after griddepcontrol.wait, when its first
+// chunk has landed, and at exit.  Never in the product build.
+#ifndef EIG33_TIMELINE
+#define EIG33_TIMELINE 0
+#endif
+#if EIG33_TIMELINE
+__device__ unsigned long long g_timeline[4096][4];
+__device__ __forceinline__ void tl_mark(int slot) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (w < 4096) g_timeline[w][slot] = t;
+  }
+}
+#else
+__device__ __forceinline__ void tl_mark(int) {}
+#endif
 
 __device__ __forceinline__ void load_tables(double* tab) {
   copy_table(tab, eig33_tab);
@@ -194,12 +249,14 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
   return L;
 }
 
-// Slow tiers of the record pipeline.  The general tier is a real call by
-// default so that its register demand never enters the allocation of the
-// steady-state loop (EIG33_GENERAL_INLINE=1 inlines it, for measurement); the
-// moderate tier is small enough to inline.
+// Slow tiers of the record pipeline.  Both are inlined: the general tier used
+// to be a real call (in reference order, with arrays, inlining it made ptxas
+// spill inside the steady-state loop and cost 3x); as straight-line any-input
+// forms it inlines with no spills and measured +20% on config 4 and +7% on
+// config 5 with flags (tools/variant_compare.py; EIG33_GENERAL_INLINE=0 keeps
+// the call).
 #ifndef EIG33_GENERAL_INLINE
-#define EIG33_GENERAL_INLINE 0
+#define EIG33_GENERAL_INLINE 1
 #endif
 #if EIG33_GENERAL_INLINE
 #define EIG33_GENERAL_ATTR __forceinline__
@@ -256,39 +313,92 @@ __device__ EIG33_GENERAL_ATTR StepOut tier_general(M9 mm, bool sym_ok, bool mod,
   return o;
 }
 
-// Per-warp record pipeline.  Work unit = a chunk of 32 consecutive records,
-// one per lane.  Lane 0 streams the warp's chunks HBM -> SMEM with
+// Per-warp record pipeline.  Work unit = a chunk of kChunk consecutive
+// records (kRPL per lane).  Lane 0 streams the warp's chunks HBM -> SMEM with
 // cp.async.bulk into a kStages-deep per-warp ring completed on per-warp
 // mbarriers: no block-wide barrier in the loop.
+//
+// Chunk assignment (EIG33_DYN=1, the default): block b owns the chunks
+// b, b + G, b + 2G, ... (G = grid size) and its warps take them from a
+// block-level SMEM counter -- each warp's first kStages chunks statically,
+// every further one with one shared-memory atomicAdd when a ring stage is
+// handed back to the TMA engine (kStages chunks ahead of use, so the atomic's
+// latency is hidden).  The warp scheduler favours some warps over others
+// (greedy-then-oldest); with a static split the favoured warps finish early
+// and the SM runs its last microseconds with too few warps to hide the FP64
+// latency.  Dynamic assignment keeps every warp busy to within one chunk of
+// the block's end.  (EIG33_DYN=0: warp gw takes chunks gw, gw + W, ...)
+#ifndef EIG33_DYN
+#define EIG33_DYN 1
+#endif
+static_assert(kStages == 2, "the chunk bookkeeping below holds exactly two ring stages");
 struct WarpRing {
   double* ring;
   unsigned long long* bars;
   const double* a;
-  long long n, nchunks, full, W;
-  int lane;
+  long long n, nchunks, full;
+  long long b, G, gw, W;  // block, grid size, global warp, total warps
+  int* next;              // block counter in SMEM
+  int warp, lane;
+  long long cid0, cid1;   // chunk of ring stage 0 / 1 (lane 0's values are authoritative)
 };
+__device__ __forceinline__ WarpRing make_ring(Smem& S, const double* a, long long n, int warp, int lane) {
+  WarpRing R;
+  R.ring = S.in[warp][0];
+  R.bars = S.bar[warp];
+  R.a = a;
+  R.n = n;
+  R.nchunks = (n + kChunk - 1) / kChunk;
+  R.full = n / kChunk;
+  R.b = blockIdx.x;
+  R.G = gridDim.x;
+  R.gw = (long long)blockIdx.x * kWarps + warp;
+  R.W = (long long)gridDim.x * kWarps;
+  R.next = &S.next;
+  R.warp = warp;
+  R.lane = lane;
+  R.cid0 = R.cid1 = 0;
+  return R;
+}
+// First chunk of ring stage s, and the chunk that follows c when its stage is
+// refilled (lane 0 only).
+__device__ __forceinline__ long long sched_first(const WarpRing& R, int s) {
+  return EIG33_DYN ? R.b + (long long)(R.warp + s * kWarps) * R.G : R.gw + (long long)s * R.W;
+}
+__device__ __forceinline__ long long sched_next(const WarpRing& R, long long c) {
+  return EIG33_DYN ? R.b + (long long)atomicAdd(R.next, 1) * R.G : c + (long long)kStages * R.W;
+}
+// thread 0, before the block barrier: the counter starts past the static chunks
+__device__ __forceinline__ void sched_init(Smem& S) {
+  if (threadIdx.x == 0) S.next = kStages * kWarps;
+}
 
 template <bool TMA>
-__device__ __forceinline__ void ring_prologue(const WarpRing& R, long long gw) {
-  if (TMA && R.lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const long long c = gw + (long long)s * R.W;
-      if (c < R.full) {
-        mbar_expect_tx(&R.bars[s], kChunkBytes);
-        EIG33_CHECK((c + 1) * kChunk <= R.n);
-        bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+__device__ __forceinline__ void ring_prologue(WarpRing& R) {
+  if (R.lane == 0) {
+    R.cid0 = sched_first(R, 0);
+    R.cid1 = sched_first(R, 1);
+    if (TMA) {
+      for (int s = 0; s < kStages; ++s) {
+        const long long c = s ? R.cid1 : R.cid0;
+        if (c < R.full) {
+          mbar_expect_tx(&R.bars[s], kChunkBytes);
+          EIG33_CHECK((c + 1) * kChunk <= R.n);
+          bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+        }
       }
     }
   }
 }
 
-// Chunk c (iteration it) of this warp: wait for its TMA (or load it
-// cooperatively: misaligned input / ragged last chunk); returns the SMEM
-// buffer and the record count.
+// Iteration it of this warp: the chunk in ring stage it % 2 (c, broadcast
+// from lane 0; nullptr when the warp's work is done); waits for its TMA (or
+// loads it cooperatively: misaligned input / ragged last chunk).
 template <bool TMA>
-__device__ __forceinline__ double* ring_acquire(const WarpRing& R, long long c, uint32_t it,
-                                                int& cnt) {
+__device__ __forceinline__ double* ring_acquire(const WarpRing& R, uint32_t it, long long& c, int& cnt) {
   const uint32_t stage = it & (kStages - 1);
+  c = __shfl_sync(0xffffffffu, stage ? R.cid1 : R.cid0, 0);
+  if (c >= R.nchunks) return nullptr;
   double* buf = R.ring + stage * (kChunk * 9);
   cnt = kChunk;
   if (TMA && c < R.full) {
@@ -317,13 +427,14 @@ __device__ __forceinline__ void ring_read(const double* buf, int lane, int h, do
   if (!mod) mod = is_moderate_or_zero(m);
 }
 template <bool TMA>
-__device__ __forceinline__ void ring_release(const WarpRing& R, long long c, uint32_t it,
-                                             double* buf) {
+__device__ __forceinline__ void ring_release(WarpRing& R, long long c, uint32_t it, double* buf) {
   __syncwarp();
-  if (TMA && R.lane == 0) {
+  if (R.lane == 0) {
     const uint32_t stage = it & (kStages - 1);
-    const long long nc = c + (long long)kStages * R.W;
-    if (nc < R.full) {
+    const long long nc = sched_next(R, c);
+    if (stage) R.cid1 = nc;
+    else R.cid0 = nc;
+    if (TMA && nc < R.full) {
       mbar_expect_tx(&R.bars[stage], kChunkBytes);
       EIG33_CHECK((nc + 1) * kChunk <= R.n);
       bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
@@ -347,21 +458,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long gw = (long long)blockIdx.x * kWarps + warp;
-  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
-             (long long)gridDim.x * kWarps, lane};
+  WarpRing R = make_ring(S, a, n, warp, lane);
 
   if (TMA && lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  sched_init(S);
+  tl_mark(0);
   pdl_trigger();
   load_tables(S.tab);
-  __syncthreads();  // tables + barrier init; the only block-wide barrier
+  __syncthreads();  // tables + barrier init + chunk counter; the only block-wide barrier
   pdl_wait();
+  tl_mark(1);
   const Tabs T{S.tab};
-  ring_prologue<TMA>(R, gw);
-  if (gw >= R.nchunks) return;
+  ring_prologue<TMA>(R);
 
   double m[9];
   bool mod, bad, pmod, pbad, pfast, pvalid;
@@ -371,12 +482,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   long long pr;  // record index of the carried stage
   constexpr bool kQueue = MODE == kEig && WANT_FLAGS;
   AdvEntry* advq = kQueue ? reinterpret_cast<AdvEntry*>(smem_raw + sizeof(Smem)) + warp * kAdvQ : nullptr;
-  uint32_t qh = 0, qt = 0;  // queue head / tail (warp-uniform)
-  auto store_stage1 = [&](long long r, bool valid) {
+  AdvRec* advr = kQueue ? reinterpret_cast<AdvRec*>(smem_raw + sizeof(Smem)) + warp * kAdvR : nullptr;
+  uint32_t qh = 0, qt = 0;  // queue head / tail (warp-uniform, monotone counts)
+  // src: this lane's record in the ring (EIG33_ADVQ_SMEM copies it into the queue)
+  auto store_stage1 = [&](long long r, bool valid, const double* src) {
     const bool pend = kQueue && valid && f == kPending;
     if (kQueue) {  // pending records go to the advisory queue, their flag byte comes later
       const unsigned pm = __ballot_sync(0xffffffffu, pend);
       if (pm) {
+#if EIG33_ADVQ_SMEM
+        if (qt + __popc(pm) > kAdvR) {
+          advisory_flush_smem(flags, advr, qt);
+          qt = 0;
+        }
+        if (pend) {
+          AdvRec& e = advr[qt + __popc(pm & ((1u << lane) - 1u))];
+#pragma unroll
+          for (int k = 0; k < 9; ++k) e.m[k] = src[k];
+          e.j2 = v.j2;
+          e.j3 = v.j3;
+          e.disc = v.disc;
+          e.idx = r;
+        }
+        qt += __popc(pm);
+#else
+        (void)src;
         if (pend) {
           const uint32_t pos = (qt + __popc(pm & ((1u << lane) - 1u))) & (kAdvQ - 1);
           advq[pos] = AdvEntry{r, v.j2, v.j3, v.disc};
@@ -386,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
           advisory_flush(a, flags, advq, qh, 32u);
           qh += 32u;
         }
+#endif
       }
     }
     if (!valid) return;
@@ -406,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     lam[pr * 3 + 2] = L.l3;
   };
   // One step of the record pipeline: stage 2 of the carried record, stage 1 of m.
-  auto step = [&](long long r, bool valid) {
+  auto step = [&](long long r, bool valid, const double* src) {
     Carry nc;
     Lam L;
     bool sym_ok = true;
@@ -450,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
     nc = Carry{v.i1, v.j2, v.j3, v.disc, m[0], m[4], m[8]};
     store_lam(L);
-    store_stage1(r, valid);
+    store_stage1(r, valid, src);
     pc = nc;
     pmod = mod;
     pfast = mod && fast_carry(v);
@@ -461,35 +592,49 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
   // ---- prologue: first chunk; stage 1 of its first record ----
   int cnt;
-  double* buf = ring_acquire<TMA>(R, gw, 0, cnt);
+  long long c;
+  double* buf = ring_acquire<TMA>(R, 0, c, cnt);
+  if (!buf) return;  // no chunk for this warp (small batch)
+  tl_mark(2);
+  // with the record-copying advisory queue the stage is handed back only
+  // after the chunk's last step has read its pending records
+  constexpr bool kLateRelease = kQueue && EIG33_ADVQ_SMEM;
   ring_read(buf, lane, 0, m, mod);
-  if (kRPL == 1) ring_release<TMA>(R, gw, 0, buf);
+  if (kRPL == 1 && !kLateRelease) ring_release<TMA>(R, c, 0, buf);
   stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
   pmod = mod;
   pfast = mod && fast_carry(v);
-  pr = gw * kChunk + lane;
+  pr = c * kChunk + lane;
   pvalid = lane < cnt;
-  store_stage1(pr, pvalid);
+  store_stage1(pr, pvalid, buf + lane * 9);
+  if (kRPL == 1 && kLateRelease) ring_release<TMA>(R, c, 0, buf);
 #pragma unroll
   for (int h = 1; h < kRPL; ++h) {
     ring_read(buf, lane, h, m, mod);
-    if (h == kRPL - 1) ring_release<TMA>(R, gw, 0, buf);
-    step(gw * kChunk + 32 * h + lane, 32 * h + lane < cnt);
+    if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, 0, buf);
+    step(c * kChunk + 32 * h + lane, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
+    if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, 0, buf);
   }
 
-  uint32_t it = 1;
-  for (long long c = gw + R.W; c < R.nchunks; c += R.W, ++it) {
-    buf = ring_acquire<TMA>(R, c, it, cnt);
+  for (uint32_t it = 1;; ++it) {
+    buf = ring_acquire<TMA>(R, it, c, cnt);
+    if (!buf) break;
     const long long base = c * kChunk + lane;
 #pragma unroll
     for (int h = 0; h < kRPL; ++h) {
       ring_read(buf, lane, h, m, mod);
-      if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
-      step(base + 32 * h, 32 * h + lane < cnt);
+      if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, it, buf);
+      step(base + 32 * h, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
+      if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, it, buf);
     }
   }
   store_lam(stage2(pc, pmod, pbad, T));
-  if (kQueue && qt != qh) advisory_flush(a, flags, advq, qh, qt - qh);
+#if EIG33_ADVQ_SMEM
+  if (kQueue && qt) advisory_flush_smem(flags, advr, qt);
+#else
+  if (kQueue && qt != qh) advisory_flush(a, flags, advq, qh, qt - qh);  // < 32 left
+#endif
+  tl_mark(3);
 }
 
 // Invariants-only kernel: stage 1 alone, same per-warp TMA ring.
@@ -500,21 +645,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long gw = (long long)blockIdx.x * kWarps + warp;
-  WarpRing R{S.in[warp][0], S.bar[warp], a, n, (n + kChunk - 1) / kChunk, n / kChunk,
-             (long long)gridDim.x * kWarps, lane};
+  WarpRing R = make_ring(S, a, n, warp, lane);
   if (TMA && lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  sched_init(S);
   pdl_trigger();
   __syncthreads();
   pdl_wait();
-  ring_prologue<TMA>(R, gw);
-  uint32_t it = 0;
-  for (long long c = gw; c < R.nchunks; c += R.W, ++it) {
+  ring_prologue<TMA>(R);
+  for (uint32_t it = 0;; ++it) {
     int cnt;
-    double* buf = ring_acquire<TMA>(R, c, it, cnt);
+    long long c;
+    double* buf = ring_acquire<TMA>(R, it, c, cnt);
+    if (!buf) break;
 #pragma unroll
     for (int h = 0; h < kRPL; ++h) {
       double m[9];

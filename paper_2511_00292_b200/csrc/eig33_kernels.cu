@@ -74,7 +74,10 @@ static int launch_fused(const double* a, size_t n, double* inv, double* lam, uin
   if (dev < 0 || dev >= 64) return fail(EIG33_EINVAL, "device index out of range");
   DevInfo& d = g_dev[dev];
   // eigvals with flags also carries the per-warp advisory queues
-  const size_t smem = sizeof(Smem) + (MODE == kEig && WF ? sizeof(AdvEntry) * kAdvQ * kWarps : 0);
+  const size_t smem = sizeof(Smem) + (MODE == kEig && WF ? (EIG33_ADVQ_SMEM ? sizeof(AdvRec) * kAdvR
+                                                                           : sizeof(AdvEntry) * kAdvQ) *
+                                                                kWarps
+                                                          : 0);
   using KernFn = void (*)(const double*, long long, double*, double*, uint8_t*);
   KernFn kern;
   if constexpr (MODE == kInv)
@@ -138,12 +141,25 @@ static int dispatch_out(const double* a, size_t n, double* inv, double* lam, uin
                : launch_fused<MODE, TMA, false, false>(a, n, inv, lam, flags, st);
 }
 
+// Launches cover at most 2^31 records (32-bit chunk bookkeeping inside the
+// kernel); larger batches -- beyond 154 GB of input, so only on future parts --
+// are cut into such pieces (each 16-B aligned if the batch is).
 template <int MODE>
 static int dispatch(const double* a, size_t n, double* inv, double* lam, uint8_t* flags,
                     cudaStream_t st) {
-  const bool aligned = ((uintptr_t)a & 15u) == 0;
-  return aligned ? dispatch_out<MODE, true>(a, n, inv, lam, flags, st)
-                 : dispatch_out<MODE, false>(a, n, inv, lam, flags, st);
+  constexpr size_t kMaxLaunch = size_t(1) << 31;
+  for (size_t lo = 0; lo < n; lo += kMaxLaunch) {
+    const size_t m = n - lo < kMaxLaunch ? n - lo : kMaxLaunch;
+    const double* ap = a + lo * 9;
+    double* ip = inv ? inv + lo * 4 : nullptr;
+    double* lp = lam ? lam + lo * 3 : nullptr;
+    uint8_t* fp = flags ? flags + lo : nullptr;
+    const bool aligned = ((uintptr_t)ap & 15u) == 0;
+    const int rc = aligned ? dispatch_out<MODE, true>(ap, m, ip, lp, fp, st)
+                           : dispatch_out<MODE, false>(ap, m, ip, lp, fp, st);
+    if (rc) return rc;
+  }
+  return EIG33_OK;
 }
 
 }  // namespace eig33b
@@ -153,6 +169,16 @@ using namespace eig33b;
 extern "C" {
 
 int eig33cu_version(void) { return (1 << 16) | 0; }
+
+#if EIG33_TIMELINE
+// diagnostic builds only (tools/timeline.py): copy k_fused's per-warp timeline out
+int eig33_debug_timeline(unsigned long long* out, int warps) {
+  return cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 4 * (warps < 4096 ? warps : 4096)) ==
+                 cudaSuccess
+             ? 0
+             : 1;
+}
+#endif
 const char* eig33cu_last_error(void) { return g_err.c_str(); }
 
 int eig33cu_invariants(const double* d_a, size_t n, double* d_inv, void* stream) {

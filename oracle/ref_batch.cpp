@@ -175,3 +175,32 @@ int ref_jacobians(const double* a, std::size_t n, double* jj2, double* jj3, doub
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// bench::generate_case (src/bench.cpp:69-75) for one path / transform over a
+// vector of deltas.  bench.cpp itself needs GMP/MPFR/Boost headers absent here,
+// so its two lines of glue are restated -- the transform constants of
+// make_transform (src/bench.cpp:52-67) and matmul(matmul(u, d), uinv) -- while
+// every rounded operation runs in the reference's own compiled mat3.cpp
+// (Mat3::diagonal, matmul, inverse_adjugate; include/eig33/mat3.hpp:32,57,69).
+// path: 0 = D1, 1 = D2; kind: 0 = Symm, 1 = U1, 2 = U2(gamma).
+int ref_generate_case(int path, int kind, double gamma, const double* deltas, std::size_t n,
+                      double* out) {
+  constexpr double q = 0x1.6a09e667f3bcdp-1;  // std::numbers::sqrt2_v<double> / 2.0 (exact halving)
+  eig33::Mat3 u;
+  if (kind == 0) u = eig33::Mat3{{q, -0.5, 0.5, q, 0.5, -0.5, 0.0, q, q}};
+  else if (kind == 1) u = eig33::Mat3{{1, -1, 1, 1, 1, 1, -1, -1, 1}};
+  else if (gamma != 0.0) u = eig33::Mat3{{1, 1, 1, 1, 0, 1, 2, 1, 2.0 + gamma}};
+  else return 2;
+  const double low = path == 0 ? 1.0 : -1.0;
+  const eig33::Mat3 uinv = eig33::inverse_adjugate(u);
+  for (std::size_t i = 0; i < n; ++i) {
+    const eig33::Mat3 d = eig33::Mat3::diagonal(low, 1.0, 1.0 + deltas[i]);
+    const eig33::Mat3 a = eig33::matmul(eig33::matmul(u, d), uinv);
+    std::memcpy(out + 9 * i, a.e.data(), 72);
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -129,11 +129,32 @@ def build_hostmath():
               "-o", out, src, "-lm"])
 
 
+REF_CXX_CHECK = os.path.join(ROOT, "tests", "cpp", "batch_api_check_ref")
+
+
+def build_ref_cxx_check():
+    """tests/cpp/batch_api_check.cpp compiled against the REFERENCE's own headers
+    (Mat3 / InvariantSet / EigenTriple / NotSymmetric from
+    /root/reference/proj/include) and linked with the product library -- built
+    here, where the reference exists, and run by the GPU suite (the GPU box has
+    no /root/reference).  Test infrastructure; git-ignored, travels with gpurun."""
+    if not os.path.isdir(os.path.join(REF, "include")):
+        return None
+    src = os.path.join(ROOT, "tests", "cpp", "batch_api_check.cpp")
+    if not _stale(REF_CXX_CHECK, [src, SO, os.path.join(ROOT, "include", "eig33", "batch.hpp"),
+                                  os.path.join(ROOT, "include", "eig33_cuda.h")]):
+        return REF_CXX_CHECK
+    _run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(REF, "include"),
+          src, "-o", REF_CXX_CHECK, SO, "-Wl,-rpath,$ORIGIN/../../paper_2511_00292_b200"])
+    return REF_CXX_CHECK
+
+
 def build_all(force=False):
     build_product(force)
     build_probes(force)
     build_oracle()
     build_hostmath()
+    build_ref_cxx_check()
 
 
 if __name__ == "__main__":

@@ -258,6 +258,9 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
 #ifndef EIG33_GENERAL_INLINE
 #define EIG33_GENERAL_INLINE 1
 #endif
+#ifndef EIG33_ROLLED
+#define EIG33_ROLLED 0
+#endif
 #if EIG33_GENERAL_INLINE
 #define EIG33_GENERAL_ATTR __forceinline__
 #else
@@ -608,6 +611,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   pvalid = lane < cnt;
   store_stage1(pr, pvalid, buf + lane * 9);
   if (kRPL == 1 && kLateRelease) ring_release<TMA>(R, c, 0, buf);
+#if EIG33_ROLLED
+  // One instance of the step code (rolled over the record slots of a chunk):
+  // the step inlines three tiers, so unrolling over kRPL slots (and peeling
+  // the first chunk) multiplied the loop's code ~3x, which the instruction
+  // cache could not hold once the tiers interleave (config 5).
+  {
+    uint32_t it = 0;
+    int h = 1;
+#pragma unroll 1
+    for (;;) {
+      if (h == kRPL) {
+        buf = ring_acquire<TMA>(R, ++it, c, cnt);
+        if (!buf) break;
+        h = 0;
+      }
+      ring_read(buf, lane, h, m, mod);
+      if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, it, buf);
+      step(c * kChunk + 32 * h + lane, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
+      if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, it, buf);
+      ++h;
+    }
+  }
+#else
 #pragma unroll
   for (int h = 1; h < kRPL; ++h) {
     ring_read(buf, lane, h, m, mod);
@@ -628,6 +654,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, it, buf);
     }
   }
+#endif
   store_lam(stage2(pc, pmod, pbad, T));
 #if EIG33_ADVQ_SMEM
   if (kQueue && qt) advisory_flush_smem(flags, advr, qt);

@@ -166,3 +166,20 @@ def test_port_generate_case_reproduces_perf_matrix():
     d = np.array([1e-14])
     U.port().orc_generate_case(1, 1, U.ctypes_double(1e-3), U.ptr(d), U.S(1), U.ptr(out))
     assert U.bit_equal(out[0], U.perf_matrix()).all()
+
+
+def test_port_generate_case_equals_compiled_reference_mat3():
+    """The port's generate_case (src/bench.cpp:53-75) equals the compiled
+    reference's own mat3 arithmetic over the same glue (ref_generate_case)."""
+    deltas = np.array([10.0 ** (-k / 4.0) for k in range(4, 65)] + [0.0, 1e-14, 0.5, 3.0])
+    R = U.ref()
+    for gamma in (1e-3, 0.75, -2.5):
+        for pi in (0, 1):
+            for ki in (0, 1, 2):
+                want = np.empty((deltas.size, 9))
+                got = np.empty((deltas.size, 9))
+                assert R.ref_generate_case(pi, ki, U.ctypes_double(gamma), U.ptr(deltas), U.S(deltas.size),
+                                           U.ptr(want)) == 0
+                U.port().orc_generate_case(pi, ki, U.ctypes_double(gamma), U.ptr(deltas), U.S(deltas.size),
+                                           U.ptr(got))
+                assert U.bit_equal(got, want).all(), (pi, ki, gamma)

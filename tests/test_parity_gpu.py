@@ -407,6 +407,19 @@ def test_cxx_batch_api_links_and_runs(tmp_path):
     assert out.returncode == 0 and out.stdout.strip() == "OK", out.stdout + out.stderr
 
 
+def test_cxx_batch_api_over_reference_types_runs():
+    """The same consumer compiled against the REFERENCE's own headers (its Mat3,
+    InvariantSet, EigenTriple and NotSymmetric; built by build() where
+    /root/reference exists, shipped prebuilt) links with the product library and
+    runs on the GPU: the drop-in overloads over the reference's real types."""
+    from paper_2511_00292_b200 import build
+
+    exe = build.REF_CXX_CHECK
+    assert os.path.exists(exe), f"{exe} missing: run __graft_entry__.build() where /root/reference exists"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "OK", out.stdout + out.stderr
+
+
 def test_variant_invariants_host_entry_equals_device():
     """eig33_invariants_variant_host (pageable direct, pageable staged) gives
     the device entry's bits for all three variants."""
@@ -667,17 +680,25 @@ def test_cuda_graph_capture_and_replay():
     assert torch.equal(fl, r.flags)
 
 
-def test_generate_case_matches_port_bitwise():
-    """Batched paper corpora (src/bench.cpp:53-82) on the device equal the C
-    restatement bit for bit for every path x transform over the reference grid."""
+def test_generate_case_matches_reference_bitwise():
+    """Batched paper corpora (src/bench.cpp:53-82) on the device equal the
+    compiled reference's own mat3 arithmetic (ref_generate_case: Mat3::diagonal,
+    matmul, inverse_adjugate from the unmodified mat3.cpp) and the C restatement,
+    bit for bit, for every path x transform over the reference grid."""
     deltas = np.array(eig.default_delta_grid() + [0.0, 1e-14, 0.5, 3.0])
-    for path, pi in eig.PATHS.items():
-        for kind, ki in eig.TRANSFORMS.items():
-            got = eig.generate_case(path, kind, deltas, gamma=1e-3).cpu().numpy()
-            want = np.empty((deltas.size, 9))
-            U.port().orc_generate_case(pi, ki, U.ctypes_double(1e-3), U.ptr(deltas), U.S(deltas.size),
-                                       U.ptr(want))
-            assert U.bit_equal(got, want).all(), (path, kind)
+    R = U.ref()
+    for gamma in (1e-3, 0.75):
+        for path, pi in eig.PATHS.items():
+            for kind, ki in eig.TRANSFORMS.items():
+                got = eig.generate_case(path, kind, deltas, gamma=gamma).cpu().numpy()
+                want = np.empty((deltas.size, 9))
+                assert R.ref_generate_case(pi, ki, U.ctypes_double(gamma), U.ptr(deltas), U.S(deltas.size),
+                                           U.ptr(want)) == 0
+                assert U.bit_equal(got, want).all(), (path, kind, gamma)
+                port = np.empty((deltas.size, 9))
+                U.port().orc_generate_case(pi, ki, U.ctypes_double(gamma), U.ptr(deltas), U.S(deltas.size),
+                                           U.ptr(port))
+                assert U.bit_equal(port, want).all(), (path, kind, gamma)
     with pytest.raises(ValueError):
         eig.generate_case("D1", "U2", deltas, gamma=0.0)
 

@@ -404,7 +404,7 @@ def time_launches(fn, stream, reps, torch):
     return e0.elapsed_time(e1) / reps
 
 
-def per_config_block(L, eig, torch, dev, stream, hbm_peak, hbm_src, fp64_peak, fp64_src, reps=20):
+def per_config_block(L, eig, torch, dev, stream, reps=20):
     """Configs 1-5 at their BASELINE sizes (config 3 at 2^22 here; its 2^28 is
     the headline): lambda only (96 B/record) and lambda + invariants + flags
     (129 B/record, what configs 1, 4 and 5 ask for).  Burst rates: 20
@@ -431,13 +431,9 @@ def per_config_block(L, eig, torch, dev, stream, hbm_peak, hbm_src, fp64_peak, f
                 fn()
             ms = time_launches(fn, stream, reps, torch)
             rate = n / (ms * 1e-3)
-            rf = roofline(rate, bpr, hbm_peak, hbm_src, fp64_peak, fp64_src)
             row[mode] = {"value": rate, "unit": UNIT, "ms_per_launch": ms, "launches": reps,
-                         "kernels_per_launch": 2 if mode == "lam_inv_flags" else 1,
-                         "roofline": {"bound": rf["bound"], "frac": rf["frac"],
-                                      "frac_hbm": rf["both"]["hbm"]["frac"],
-                                      "frac_fp64": rf["both"]["fp64"]["frac"],
-                                      "bytes_per_record": bpr}}
+                         "kernels_per_launch": 1,
+                         "roofline": {"bytes_per_record": bpr}}  # fractions filled in after the FP64 probe
         if cfg == 4 or cfg == 5:
             adv = int((fl.to(torch.int32) & 1).sum().item())
             row["advisory_share"] = adv / n
@@ -631,12 +627,6 @@ def run_ours(args, rank, world, local_rank):
         sustained = {"value": n_total / (ms_sus * 1e-3), "unit": UNIT, "seconds": max(mss) / 1e3,
                      "launches_per_rank": ks, "ms_per_step": ms_sus}
         barrier()
-    # FP64 issue-rate peaks on this GPU (roofline denominators), measured after
-    # the timed regions so that their full-power DFMA bursts do not precede
-    # the workload: burst (for the short headline region) and sustained
-    # chaotic-operand DFMA (for the long run)
-    fp64_burst = P.eig33_probe_fp64_rate(20)
-    fp64_sus = P.eig33_probe_fp64_chaos(2.5) if args.sustained_seconds > 0 else 0.0
 
     # ---- e2e: the same shard through the public host-buffer API, pinned ----
     e2e = None
@@ -698,8 +688,7 @@ def run_ours(args, rank, world, local_rank):
                   "(tools/probes eig33_probe_fp64_chaos)")
     per_config = None
     if not args.no_per_config and rank == 0:
-        per_config = per_config_block(L, eig, torch, dev, stream, hbm_peak, hbm_src,
-                                      fp64_burst / 1e12, fp64_src_b)
+        per_config = per_config_block(L, eig, torch, dev, stream)
     barrier()
 
     # ---- multi-driver: one process, eig33_multi_eigvals over N devices ----
@@ -708,7 +697,9 @@ def run_ours(args, rank, world, local_rank):
         del a, lam
         torch.cuda.empty_cache()
         barrier()
-        if rank == 0:
+        if rank == 0 and torch.cuda.device_count() < world:
+            multi = {"skipped": f"rank 0 sees {torch.cuda.device_count()} devices, fewer than {world}"}
+        elif rank == 0:
             if h_a is None:  # N>1: the whole batch on rank 0's host, pinned
                 h_a = torch.empty((n_total, 9), dtype=torch.float64, pin_memory=True)
                 h_l = torch.empty((n_total, 3), dtype=torch.float64, pin_memory=True)
@@ -734,6 +725,25 @@ def run_ours(args, rank, world, local_rank):
                             "pinned host buffers); wall clock"}
         barrier()
     h_a = h_l = None
+
+    # FP64 issue-rate peaks on this GPU (roofline denominators), measured last so
+    # that their full-power DFMA does not precede the workload, each after 2 s
+    # idle: burst (11 ms launches, for the short headline region and the
+    # per-config launches) and sustained chaotic-operand DFMA over 2.5 s (for
+    # the sustained sub-run)
+    time.sleep(2.0)
+    fp64_burst = P.eig33_probe_fp64_rate(20)
+    fp64_sus = 0.0
+    if args.sustained_seconds > 0:
+        time.sleep(2.0)
+        fp64_sus = P.eig33_probe_fp64_chaos(2.5)
+    if per_config:
+        for row in per_config.values():
+            for mode in ("lam", "lam_inv_flags"):
+                rf = roofline(row[mode]["value"], row[mode]["roofline"]["bytes_per_record"], hbm_peak, hbm_src,
+                              fp64_burst / 1e12, fp64_src_b)
+                row[mode]["roofline"].update(bound=rf["bound"], frac=rf["frac"], frac_hbm=rf["both"]["hbm"]["frac"],
+                                             frac_fp64=rf["both"]["fp64"]["frac"])
 
     clocks.stop()
     if rank != 0:

@@ -23,6 +23,9 @@ import torch  # noqa: E402
 import paper_2511_00292_b200 as eig  # noqa: E402
 
 L = eig.lib()
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..'))
+import bench  # noqa: E402
+PR = bench.probes_lib()  # measurement probes: tools/probes/libeig33_probes.so (not the product)
 
 
 def sample(fn, secs=3.0):
@@ -51,12 +54,12 @@ def main():
     pa, pl = ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(lam.data_ptr())
     tag = os.environ.get("TAG", "product")
     if tag == "memonly":
-        L.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
-        clk, pw, r = sample(lambda: L.eig33_probe_memonly(pa, n, pl, st))
+        PR.eig33_probe_memonly.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
+        clk, pw, r = sample(lambda: PR.eig33_probe_memonly(pa, n, pl, st))
     elif tag == "stream":
-        L.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+        PR.eig33_probe_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
                                          ctypes.c_void_p]
-        clk, pw, r = sample(lambda: L.eig33_probe_stream(pa, n, pl, st))
+        clk, pw, r = sample(lambda: PR.eig33_probe_stream(pa, n, pl, st))
     else:
         clk, pw, r = sample(lambda: L.eig33cu_eigvals(pa, n, None, pl, None, st))
     print(f"{tag:10s} clk {clk:.0f} MHz power {pw:.0f} W  {r * n / 1e9:.1f} G rec/s"

@@ -6,6 +6,9 @@ import torch
 import paper_2511_00292_b200 as eig
 
 L = eig.lib()
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..'))
+import bench  # noqa: E402
+PR = bench.probes_lib()  # measurement probes: tools/probes/libeig33_probes.so (not the product)
 
 
 def sample(fn, secs=3.0):
@@ -27,9 +30,9 @@ def sample(fn, secs=3.0):
     return clk, pw, n / el
 
 
-L.eig33_probe_fp64_op.restype = ctypes.c_double
-L.eig33_probe_fp64_op.argtypes = [ctypes.c_int] * 3
-print("dfma    clk %.0f MHz  power %.0f W  calls/s %.1f" % sample(lambda: L.eig33_probe_fp64_op(0, 20, 8192)))
+PR.eig33_probe_fp64_op.restype = ctypes.c_double
+PR.eig33_probe_fp64_op.argtypes = [ctypes.c_int] * 3
+print("dfma    clk %.0f MHz  power %.0f W  calls/s %.1f" % sample(lambda: PR.eig33_probe_fp64_op(0, 20, 8192)))
 x = torch.empty(1 << 31, dtype=torch.uint8, device="cuda")
 y = torch.empty_like(x)
 clk, pw, r = sample(lambda: y.copy_(x))

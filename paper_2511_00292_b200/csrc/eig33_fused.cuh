@@ -316,6 +316,23 @@ __device__ EIG33_GENERAL_ATTR StepOut tier_general(M9 mm, bool sym_ok, bool mod,
   return o;
 }
 
+// One record's invariants {i1, j2, j3, disc}: a single 256-bit store
+// (STG.256, sm_100) when the output is 32-B aligned -- a warp then writes
+// 1 KB of whole sectors -- else four 8-B stores.
+__device__ __forceinline__ void store_inv(double* __restrict__ inv, long long r, const Inv& v, bool a32) {
+  double* p = inv + r * 4;
+  if (a32) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.i1), "d"(v.j2), "d"(v.j3),
+                 "d"(v.disc)
+                 : "memory");
+  } else {
+    p[0] = v.i1;
+    p[1] = v.j2;
+    p[2] = v.j3;
+    p[3] = v.disc;
+  }
+}
+
 // Per-warp record pipeline.  Work unit = a chunk of kChunk consecutive
 // records (kRPL per lane).  Lane 0 streams the warp's chunks HBM -> SMEM with
 // cp.async.bulk into a kStages-deep per-warp ring completed on per-warp
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpRing R = make_ring(S, a, n, warp, lane);
+  const bool inv32 = ((uintptr_t)inv & 31u) == 0;
 
   if (TMA && lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
@@ -524,12 +542,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
     if (!valid) return;
     EIG33_CHECK(r >= 0 && r < R.n);
-    if (WANT_INV) {
-      inv[r * 4 + 0] = v.i1;
-      inv[r * 4 + 1] = v.j2;
-      inv[r * 4 + 2] = v.j3;
-      inv[r * 4 + 3] = v.disc;
-    }
+    if (WANT_INV) store_inv(inv, r, v, inv32);
     if (MODE != kInv && WANT_FLAGS && !pend) flags[r] = f;
   };
   auto store_lam = [&](const Lam& L) {
@@ -673,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpRing R = make_ring(S, a, n, warp, lane);
+  const bool inv32 = ((uintptr_t)inv & 31u) == 0;
   if (TMA && lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&R.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -696,10 +710,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       const Inv v = invariants_warp(m, mod, 0xffffffffu);
       if (lane + 32 * h < cnt) {
         const long long r = c * kChunk + 32 * h + lane;
-        inv[r * 4 + 0] = v.i1;
-        inv[r * 4 + 1] = v.j2;
-        inv[r * 4 + 2] = v.j3;
-        inv[r * 4 + 3] = v.disc;
+        store_inv(inv, r, v, inv32);
       }
     }
   }

@@ -202,6 +202,30 @@ def test_misaligned_input_uses_coalesced_path():
     _assert_parity(a, r.lam.cpu().numpy(), r.inv.cpu().numpy(), r.flags.cpu().numpy(), "misaligned")
 
 
+def test_unaligned_invariants_output_equals_aligned():
+    """Invariant outputs that are not 32-B aligned take four 8-B stores instead
+    of one 256-bit store: same bits, both entry points, ragged sizes."""
+    L = eig.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    for n in (1, 31, 4099, (1 << 20) + 3):
+        a_d = eig.generate(5, n, seed=n)
+        lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        fl = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ref = eig.eigvals(a_d, return_invariants=True).inv
+        for off in (8, 16, 24):
+            buf = torch.zeros(n * 4 + 4, dtype=torch.float64, device="cuda")
+            p = ctypes.c_void_p(buf.data_ptr() + off)
+            assert L.eig33cu_eigvals(P(a_d), n, p, P(lam), P(fl), st) == 0
+            got = buf[off // 8: off // 8 + 4 * n].view(n, 4)
+            torch.cuda.synchronize()
+            assert U.bit_equal(got.cpu().numpy(), ref.cpu().numpy()).all(), (n, off)
+            buf.zero_()
+            assert L.eig33cu_invariants(P(a_d), n, p, st) == 0
+            torch.cuda.synchronize()
+            assert U.bit_equal(got.cpu().numpy(), ref.cpu().numpy()).all(), (n, off, "invariants")
+
+
 def test_invariants_only_entry_point():
     a_d = eig.generate(5, 1 << 21, seed=9)
     inv = eig.invariants(a_d).cpu().numpy()

@@ -22,6 +22,20 @@ for n in (1, 33, 64, 65, 1000, 4099):
 for cfg in range(1, 6):
     g = eig.generate(cfg, 3000, seed=cfg)
     eig.eigvals(g, return_flags=True)
+# many chunks per block (dynamic chunk counter) with a ragged last chunk, and an
+# invariants output that is not 32-B aligned (scalar-store path)
+import ctypes  # noqa: E402
+L = eig.lib()
+for n in ((3 << 20) + 5, 100003):
+    g = eig.generate(5, n, seed=7)
+    lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    invb = torch.empty(n * 4 + 1, dtype=torch.float64, device="cuda")
+    fl = torch.empty(n, dtype=torch.uint8, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.eig33cu_eigvals(P(g), n, ctypes.c_void_p(invb.data_ptr() + 8), P(lam), P(fl), st) == 0
+    assert L.eig33cu_invariants(P(g), n, ctypes.c_void_p(invb.data_ptr() + 8), st) == 0
+    torch.cuda.synchronize()
 j3 = torch.randn(1000, dtype=torch.float64, device="cuda")
 eig.triple_angle(j3, torch.randn(1000, dtype=torch.float64, device="cuda"))
 a = U.mixed_corpus(2000, 3)

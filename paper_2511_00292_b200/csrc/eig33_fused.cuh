@@ -393,22 +393,37 @@ __device__ __forceinline__ void sched_init(Smem& S) {
   if (threadIdx.x == 0) S.next = kStages * kWarps;
 }
 
+// EIG33_LAZY2=1 (default): at launch each warp asks only for its first chunk;
+// the second ring stage is requested once the first has landed (ring_kick).
+// Every warp of the grid requests its first bytes at the same moment, so
+// halving that burst brings the first chunks in sooner (latest first chunk of
+// a 2^18-record launch 4.1 -> 2.8 us after griddepcontrol.wait; +0.5-1% on
+// configs 2-5, tools/variant_compare.py).
+#ifndef EIG33_LAZY2
+#define EIG33_LAZY2 1
+#endif
+template <bool TMA>
+__device__ __forceinline__ void ring_issue(const WarpRing& R, int s) {
+  const long long c = s ? R.cid1 : R.cid0;
+  if (TMA && c < R.full) {
+    mbar_expect_tx(&R.bars[s], kChunkBytes);
+    EIG33_CHECK((c + 1) * kChunk <= R.n);
+    bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+  }
+}
 template <bool TMA>
 __device__ __forceinline__ void ring_prologue(WarpRing& R) {
   if (R.lane == 0) {
     R.cid0 = sched_first(R, 0);
     R.cid1 = sched_first(R, 1);
-    if (TMA) {
-      for (int s = 0; s < kStages; ++s) {
-        const long long c = s ? R.cid1 : R.cid0;
-        if (c < R.full) {
-          mbar_expect_tx(&R.bars[s], kChunkBytes);
-          EIG33_CHECK((c + 1) * kChunk <= R.n);
-          bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
-        }
-      }
-    }
+    ring_issue<TMA>(R, 0);
+    if (!EIG33_LAZY2) ring_issue<TMA>(R, 1);
   }
+}
+// the deferred second stage (EIG33_LAZY2), after the first chunk has landed
+template <bool TMA>
+__device__ __forceinline__ void ring_kick(const WarpRing& R) {
+  if (EIG33_LAZY2 && R.lane == 0) ring_issue<TMA>(R, 1);
 }
 
 // Iteration it of this warp: the chunk in ring stage it % 2 (c, broadcast
@@ -611,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   long long c;
   double* buf = ring_acquire<TMA>(R, 0, c, cnt);
   if (!buf) return;  // no chunk for this warp (small batch)
+  ring_kick<TMA>(R);
   tl_mark(2);
   // with the record-copying advisory queue the stage is handed back only
   // after the chunk's last step has read its pending records
@@ -701,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     long long c;
     double* buf = ring_acquire<TMA>(R, it, c, cnt);
     if (!buf) break;
+    if (it == 0) ring_kick<TMA>(R);
 #pragma unroll
     for (int h = 0; h < kRPL; ++h) {
       double m[9];

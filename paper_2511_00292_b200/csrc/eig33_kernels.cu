@@ -4,21 +4,19 @@
 // MUST be compiled with --fmad=false: the invariant arithmetic is bit-exact
 // against the reference only without contraction (proj/src/CMakeLists.txt:9-10).
 //
-// Kernel map
-//   k_fused<MODE,TMA,INV,FLAGS>  persistent eigvals / eigvalss kernel.  Work
-//       unit: a 64-record chunk (4608 B), two records per lane.  Each warp owns
-//       a 2-deep SMEM ring that lane 0 fills with cp.async.bulk (TMA 1D) on
-//       per-warp mbarriers -- no block barrier in the loop.  The record loop is
-//       software-pipelined: one step = eigenvalue stage of the previous record
-//       + invariants of the next, in one branch-free block (tier A); warps
-//       with records outside that domain take the moderate tier (inlined) or
-//       the general tier (an out-of-line call), chosen per warp.  Launched with
-//       programmatic dependent launch.  Outputs are stored straight from
-//       registers.
-//   k_invariants<TMA>            invariants only, same ring.
-//   (non_real_advisory: k_fused's eigvals-with-flags form queues the records
-//       with disc < 0 per warp and evaluates disc_tolerance for them 32 at a
-//       time, bit-exact -- see AdvEntry / advisory_flush in eig33_fused.cuh.)
+// Kernel map (device code in eig33_fused.cuh)
+//   k_fused<MODE,TMA,INV,FLAGS>  persistent eigvals / eigvalss kernel: one
+//       512-thread block per SM whose warps take 64-record chunks from a
+//       block-level counter.  Each warp owns a 2-deep SMEM ring that lane 0
+//       fills with cp.async.bulk (TMA 1D) on per-warp mbarriers -- no block
+//       barrier in the loop.  The record loop is software-pipelined: one step =
+//       eigenvalue stage of the previous record + invariants of the next, in one
+//       block; the tier (steady / moderate / general, all inlined) is chosen per
+//       warp.  With flags, the records with disc < 0 are queued per warp and
+//       their non_real_advisory evaluated 32 at a time (advisory_flush).
+//       Launched with programmatic dependent launch; outputs stored straight
+//       from registers (invariants as one 256-bit store per record).
+//   k_invariants<TMA>            invariants only, same ring and scheduler.
 //   k_triple_angle               batched triple_angle.
 #include <cuda_runtime.h>
 #include <stdint.h>

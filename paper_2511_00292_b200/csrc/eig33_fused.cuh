@@ -258,9 +258,7 @@ __device__ __forceinline__ Lam stage2(const Carry& c, bool mod, bool bad, const 
 #ifndef EIG33_GENERAL_INLINE
 #define EIG33_GENERAL_INLINE 1
 #endif
-#ifndef EIG33_ROLLED
-#define EIG33_ROLLED 0
-#endif
+
 #if EIG33_GENERAL_INLINE
 #define EIG33_GENERAL_ATTR __forceinline__
 #else
@@ -352,11 +350,20 @@ __device__ __forceinline__ void store_inv(double* __restrict__ inv, long long r,
 #define EIG33_DYN 1
 #endif
 static_assert(kStages == 2, "the chunk bookkeeping below holds exactly two ring stages");
+// Chunk geometry.  Chunk ids [0, n64 - ts) are 64-record chunks; the last ts
+// full chunks are cut into 2*ts 32-record half-chunks (EIG33_SPLIT_TAIL chunks
+// per warp of the grid: the block counter hands them out last, so a launch
+// ends on half-size work units and its SMs finish closer together); a ragged
+// remainder of n % 64 records is the last chunk (no TMA).  "full" counts the
+// TMA-able chunks (64- or 32-record).
+#ifndef EIG33_SPLIT_TAIL
+#define EIG33_SPLIT_TAIL 0
+#endif
 struct WarpRing {
   double* ring;
   unsigned long long* bars;
   const double* a;
-  long long n, nchunks, full;
+  long long n, nchunks, full, n64, ts;
   long long b, G, gw, W;  // block, grid size, global warp, total warps
   int* next;              // block counter in SMEM
   int warp, lane;
@@ -368,8 +375,14 @@ __device__ __forceinline__ WarpRing make_ring(Smem& S, const double* a, long lon
   R.bars = S.bar[warp];
   R.a = a;
   R.n = n;
-  R.nchunks = (n + kChunk - 1) / kChunk;
-  R.full = n / kChunk;
+  R.n64 = n / kChunk;
+  R.ts = 0;
+  if (EIG33_SPLIT_TAIL > 0 && kRPL == 2) {
+    const long long want = (long long)EIG33_SPLIT_TAIL * kWarps * gridDim.x;
+    R.ts = want < R.n64 ? want : R.n64;
+  }
+  R.full = R.n64 + R.ts;
+  R.nchunks = R.full + (n % kChunk ? 1 : 0);
   R.b = blockIdx.x;
   R.G = gridDim.x;
   R.gw = (long long)blockIdx.x * kWarps + warp;
@@ -379,6 +392,18 @@ __device__ __forceinline__ WarpRing make_ring(Smem& S, const double* a, long lon
   R.lane = lane;
   R.cid0 = R.cid1 = 0;
   return R;
+}
+// first record and record count of chunk c (c < nchunks)
+__device__ __forceinline__ long long chunk_start(const WarpRing& R, long long c) {
+  const long long c64 = R.n64 - R.ts;
+  if (c < c64) return c * kChunk;
+  if (c < R.full) return c64 * kChunk + (c - c64) * 32;
+  return R.n64 * kChunk;
+}
+__device__ __forceinline__ int chunk_cnt(const WarpRing& R, long long c) {
+  if (c < R.n64 - R.ts) return kChunk;
+  if (c < R.full) return 32;
+  return (int)(R.n - R.n64 * kChunk);
 }
 // First chunk of ring stage s, and the chunk that follows c when its stage is
 // refilled (lane 0 only).
@@ -406,9 +431,11 @@ template <bool TMA>
 __device__ __forceinline__ void ring_issue(const WarpRing& R, int s) {
   const long long c = s ? R.cid1 : R.cid0;
   if (TMA && c < R.full) {
-    mbar_expect_tx(&R.bars[s], kChunkBytes);
-    EIG33_CHECK((c + 1) * kChunk <= R.n);
-    bulk_load(R.ring + s * (kChunk * 9), R.a + c * (kChunk * 9), kChunkBytes, &R.bars[s]);
+    const long long st = chunk_start(R, c);
+    const uint32_t bytes = (uint32_t)chunk_cnt(R, c) * 72u;
+    mbar_expect_tx(&R.bars[s], bytes);
+    EIG33_CHECK(st + chunk_cnt(R, c) <= R.n);
+    bulk_load(R.ring + s * (kChunk * 9), R.a + st * 9, bytes, &R.bars[s]);
   }
 }
 template <bool TMA>
@@ -430,17 +457,17 @@ __device__ __forceinline__ void ring_kick(const WarpRing& R) {
 // from lane 0; nullptr when the warp's work is done); waits for its TMA (or
 // loads it cooperatively: misaligned input / ragged last chunk).
 template <bool TMA>
-__device__ __forceinline__ double* ring_acquire(const WarpRing& R, uint32_t it, long long& c, int& cnt) {
+__device__ __forceinline__ double* ring_acquire(const WarpRing& R, uint32_t it, long long& c, long long& base,
+                                                int& cnt) {
   const uint32_t stage = it & (kStages - 1);
   c = __shfl_sync(0xffffffffu, stage ? R.cid1 : R.cid0, 0);
   if (c >= R.nchunks) return nullptr;
   double* buf = R.ring + stage * (kChunk * 9);
-  cnt = kChunk;
+  base = chunk_start(R, c);
+  cnt = chunk_cnt(R, c);
   if (TMA && c < R.full) {
     mbar_wait(&R.bars[stage], (it / kStages) & 1u);
   } else {
-    const long long base = c * kChunk;
-    cnt = (int)min((long long)kChunk, R.n - base);
     const double* src = R.a + base * 9;
 #pragma unroll
     for (int j = 0; j < 9 * kRPL; ++j) {
@@ -470,9 +497,11 @@ __device__ __forceinline__ void ring_release(WarpRing& R, long long c, uint32_t 
     if (stage) R.cid1 = nc;
     else R.cid0 = nc;
     if (TMA && nc < R.full) {
-      mbar_expect_tx(&R.bars[stage], kChunkBytes);
-      EIG33_CHECK((nc + 1) * kChunk <= R.n);
-      bulk_load(buf, R.a + nc * (kChunk * 9), kChunkBytes, &R.bars[stage]);
+      const long long st = chunk_start(R, nc);
+      const uint32_t bytes = (uint32_t)chunk_cnt(R, nc) * 72u;
+      mbar_expect_tx(&R.bars[stage], bytes);
+      EIG33_CHECK(st + chunk_cnt(R, nc) <= R.n);
+      bulk_load(buf, R.a + st * 9, bytes, &R.bars[stage]);
     }
   }
 }
@@ -623,8 +652,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
   // ---- prologue: first chunk; stage 1 of its first record ----
   int cnt;
-  long long c;
-  double* buf = ring_acquire<TMA>(R, 0, c, cnt);
+  long long c, base;
+  double* buf = ring_acquire<TMA>(R, 0, c, base, cnt);
   if (!buf) return;  // no chunk for this warp (small batch)
   ring_kick<TMA>(R);
   tl_mark(2);
@@ -636,54 +665,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   stage1<MODE, WANT_FLAGS>(m, mod, v, pc, f, pbad);
   pmod = mod;
   pfast = mod && fast_carry(v);
-  pr = c * kChunk + lane;
+  pr = base + lane;
   pvalid = lane < cnt;
   store_stage1(pr, pvalid, buf + lane * 9);
   if (kRPL == 1 && kLateRelease) ring_release<TMA>(R, c, 0, buf);
-#if EIG33_ROLLED
-  // One instance of the step code (rolled over the record slots of a chunk):
-  // the step inlines three tiers, so unrolling over kRPL slots (and peeling
-  // the first chunk) multiplied the loop's code ~3x, which the instruction
-  // cache could not hold once the tiers interleave (config 5).
-  {
-    uint32_t it = 0;
-    int h = 1;
-#pragma unroll 1
-    for (;;) {
-      if (h == kRPL) {
-        buf = ring_acquire<TMA>(R, ++it, c, cnt);
-        if (!buf) break;
-        h = 0;
-      }
-      ring_read(buf, lane, h, m, mod);
-      if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, it, buf);
-      step(c * kChunk + 32 * h + lane, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
-      if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, it, buf);
-      ++h;
+  // Record slot h of the current chunk: one pipeline step; a slot past the
+  // chunk's records (a 32-record half chunk) is skipped, warp-uniformly.
+  auto slot = [&](int h, uint32_t it) {
+    const bool last = h == kRPL - 1;
+    if (32 * h >= cnt) {
+      if (last) ring_release<TMA>(R, c, it, buf);
+      return;
     }
-  }
-#else
-#pragma unroll
-  for (int h = 1; h < kRPL; ++h) {
     ring_read(buf, lane, h, m, mod);
-    if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, 0, buf);
-    step(c * kChunk + 32 * h + lane, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
-    if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, 0, buf);
-  }
-
-  for (uint32_t it = 1;; ++it) {
-    buf = ring_acquire<TMA>(R, it, c, cnt);
-    if (!buf) break;
-    const long long base = c * kChunk + lane;
+    if (last && !kLateRelease) ring_release<TMA>(R, c, it, buf);
+    step(base + 32 * h + lane, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
+    if (last && kLateRelease) ring_release<TMA>(R, c, it, buf);
+  };
 #pragma unroll
-    for (int h = 0; h < kRPL; ++h) {
-      ring_read(buf, lane, h, m, mod);
-      if (h == kRPL - 1 && !kLateRelease) ring_release<TMA>(R, c, it, buf);
-      step(base + 32 * h, 32 * h + lane < cnt, buf + (lane + 32 * h) * 9);
-      if (h == kRPL - 1 && kLateRelease) ring_release<TMA>(R, c, it, buf);
-    }
+  for (int h = 1; h < kRPL; ++h) slot(h, 0);
+  for (uint32_t it = 1;; ++it) {
+    buf = ring_acquire<TMA>(R, it, c, base, cnt);
+    if (!buf) break;
+#pragma unroll
+    for (int h = 0; h < kRPL; ++h) slot(h, it);
   }
-#endif
   store_lam(stage2(pc, pmod, pbad, T));
 #if EIG33_ADVQ_SMEM
   if (kQueue && qt) advisory_flush_smem(flags, advr, qt);
@@ -714,21 +720,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   ring_prologue<TMA>(R);
   for (uint32_t it = 0;; ++it) {
     int cnt;
-    long long c;
-    double* buf = ring_acquire<TMA>(R, it, c, cnt);
+    long long c, base;
+    double* buf = ring_acquire<TMA>(R, it, c, base, cnt);
     if (!buf) break;
     if (it == 0) ring_kick<TMA>(R);
 #pragma unroll
     for (int h = 0; h < kRPL; ++h) {
+      if (32 * h >= cnt) {  // half chunk
+        if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
+        continue;
+      }
       double m[9];
       bool mod;
       ring_read(buf, lane, h, m, mod);
       if (h == kRPL - 1) ring_release<TMA>(R, c, it, buf);
       const Inv v = invariants_warp(m, mod, 0xffffffffu);
-      if (lane + 32 * h < cnt) {
-        const long long r = c * kChunk + 32 * h + lane;
-        store_inv(inv, r, v, inv32);
-      }
+      if (lane + 32 * h < cnt) store_inv(inv, base + 32 * h + lane, v, inv32);
     }
   }
 }

@@ -522,6 +522,54 @@ def power_model(P, clocks, pa, pl, n, st, stream, dev, torch):
 
 
 # ---------------------------------------------------------------------------
+class HostSync:
+    """Rank plumbing shared by the GPU arm and the dry run: the default process
+    group (NCCL on the GPU arm, as the contract asks; gloo in the dry run) plus a
+    gloo group that carries every host-side barrier and reduction -- an NCCL
+    barrier would leave a spinning kernel on a waiting rank's GPU while rank 0
+    drives all devices in the multi-driver leg."""
+
+    def __init__(self, world, backend, device=None):
+        self.world = world
+        self.dist = self.pg = None
+        if world > 1:
+            import torch.distributed as dist
+
+            if device is not None:
+                dist.init_process_group(backend, device_id=device)
+            else:
+                dist.init_process_group(backend)
+            self.dist = dist
+            self.pg = dist.new_group(backend="gloo")
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier(group=self.pg)
+
+    def gather(self, x):
+        """all ranks' float x, in rank order"""
+        if self.dist is None:
+            return [float(x)]
+        import torch
+
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.pg)
+        return [float(o.item()) for o in out]
+
+    def gather_obj(self, x):
+        if self.dist is None:
+            return [x]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, x, group=self.pg)
+        return out
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -532,34 +580,8 @@ def run_ours(args, rank, world, local_rank):
         raise SystemExit("--warmup must be >= 3")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist = hostpg = None
-    if world > 1:
-        import torch.distributed as dist  # noqa: F811
-
-        dist.init_process_group("nccl", device_id=dev)
-        # Host-side synchronisation goes through a gloo group: an NCCL barrier
-        # would leave a spinning kernel on the waiting ranks' GPUs while rank 0
-        # drives all devices in the multi-driver leg.
-        hostpg = dist.new_group(backend="gloo")
-
-    def barrier():
-        if dist is not None:
-            dist.barrier(group=hostpg)
-
-    def gather(x):
-        if dist is None:
-            return [float(x)]
-        t = torch.tensor([float(x)], dtype=torch.float64)
-        out = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(out, t, group=hostpg)
-        return [float(o.item()) for o in out]
-
-    def gather_int(x):
-        if dist is None:
-            return [x]
-        out = [None] * world
-        dist.all_gather_object(out, x, group=hostpg)
-        return out
+    sync = HostSync(world, "nccl", dev)
+    barrier, gather, gather_int = sync.barrier, sync.gather, sync.gather_obj
 
     L = eig.lib()
     P = probes_lib()
@@ -747,8 +769,7 @@ def run_ours(args, rank, world, local_rank):
 
     clocks.stop()
     if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
+        sync.close()
         return
 
     per_gpu = value / world
@@ -805,40 +826,33 @@ def run_ours(args, rank, world, local_rank):
                                   "spec_at_max_clock": SPEC_FP64_INST_PER_S},
     }
     print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    sync.close()
 
 
 def run_dry(args, rank, world):
-    """CPU-only check of the N-rank harness (gloo): the shard each rank owns,
-    the max-over-ranks timing reduction and the JSON line's shape.  No kernel
-    runs; the 'step' is a fixed host sleep per record so rank times differ."""
-    import torch
-    import torch.distributed as dist
-
-    if world > 1:
-        dist.init_process_group("gloo")
+    """CPU-only check of the N-rank harness (gloo): the same HostSync plumbing,
+    shard of each rank, max-over-ranks timing reduction and JSON line shape as
+    the GPU arm.  No kernel runs; the 'step' is a host sleep proportional to the
+    rank's shard so rank times differ."""
+    sync = HostSync(world, "gloo")
     lo, hi = shard_of(args.records, world, rank)
+    sync.barrier()
     t0 = time.perf_counter()
     for _ in range(args.warmup + args.steps):
         time.sleep((hi - lo) * 1e-9)
     ms = (time.perf_counter() - t0) * 1e3 * args.steps / (args.warmup + args.steps)
-    t = torch.tensor([ms, float(lo), float(hi)], dtype=torch.float64)
-    out = [torch.zeros_like(t) for _ in range(world)]
-    if world > 1:
-        dist.all_gather(out, t)
-    else:
-        out = [t]
+    per = sync.gather(ms)
+    shards = sync.gather_obj([lo, hi])
+    cks = sync.gather_obj(rank + 1)
+    sync.barrier()
     if rank == 0:
-        per = [float(o[0]) for o in out]
-        shards = [[int(o[1]), int(o[2])] for o in out]
         print(json.dumps({"impl": "dry-run", "metric": METRIC, "value": args.records * args.steps / (max(per) * 1e-3),
                           "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                           "ms_per_step": max(per) / args.steps, "higher_is_better": True, "scaling": "strong",
-                          "per_rank_ms": per, "shards": shards, "config": config_block(args.records, world)}),
+                          "per_rank_ms": per, "shards": shards, "rank_objects": cks,
+                          "config": config_block(args.records, world)}),
               flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    sync.close()
 
 
 def main():

@@ -84,4 +84,5 @@ def test_torchrun_strong_sharding_dry_run(world):
     assert shards[0][0] == 0 and shards[-1][1] == n
     assert all(b[0] == a[1] for a, b in zip(shards, shards[1:]))
     assert d["config"]["records_per_gpu"] == [hi - lo for lo, hi in shards]
+    assert d["rank_objects"] == list(range(1, world + 1))  # all_gather_object over the gloo group
     assert sum(d["config"]["records_per_gpu"]) == n == d["config"]["records_total"]

@@ -73,7 +73,13 @@ struct AdvEntry {
   long long idx;
   double j2, j3, disc;
 };
-constexpr uint32_t kAdvQ = 64;  // entries per warp (power of two, >= 2 x 32)
+#ifndef EIG33_ADV_FUSED
+#define EIG33_ADV_FUSED 0
+#endif
+// entries per warp: >= 2 x 32 (flush at 32); with EIG33_ADV_FUSED the moderate
+// tier consumes 32 whenever it can and the separate flush waits for 64
+constexpr uint32_t kAdvQ = EIG33_ADV_FUSED ? 96 : 64;
+constexpr uint32_t kAdvFlushAt = EIG33_ADV_FUSED ? 64 : 32;
 
 // Evaluate `count` (<= 32) queued records starting at `head`, one per lane,
 // and write their final flag bytes.  Out of line: its registers never enter
@@ -83,7 +89,7 @@ __device__ __noinline__ void advisory_flush(const double* __restrict__ a, uint8_
   __syncwarp();  // queue entries were written by other lanes
   const uint32_t lane = threadIdx.x & 31u;
   if (lane < count) {
-    const AdvEntry e = q[(head + lane) & (kAdvQ - 1)];
+    const AdvEntry e = q[(head + lane) % kAdvQ];
     EIG33_CHECK(e.idx >= 0);
     double m[9];
 #pragma unroll
@@ -284,6 +290,29 @@ __device__ __forceinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* 
   StepOut o;
   o.L = eig_moderate_bl(pc, tab);
   o.v = invariants_moderate(mm.e);
+  o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
+  o.bad = false;
+  o.mod = true;
+  return o;
+}
+
+// EIG33_ADV_FUSED=1 (measurement variant): when the advisory queue holds >= 32
+// records and the step takes the moderate tier, the 32 advisories are evaluated
+// inside the tier's basic block (one queued record per lane, its 72 B read from
+// L2 at the top), so their dependent chains interleave with the step's DAG
+// instead of running as a separate latency-bound flush.
+template <int MODE, bool WANT_FLAGS>
+__device__ __forceinline__ StepOut tier_moderate_adv(M9 mm, Carry pc, const double* tab,
+                                                     const double* __restrict__ a, uint8_t* __restrict__ flags,
+                                                     long long qidx, double qj2, double qj3, double qdisc) {
+  double qm[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) qm[k] = __ldg(a + qidx * 9 + k);
+  StepOut o;
+  o.L = eig_moderate_bl(pc, tab);
+  o.v = invariants_moderate(mm.e);
+  const bool adv = advisory(qm, Inv{0.0, qj2, qj3, qdisc});
+  flags[qidx] = adv ? EIG33_FLAG_ADVISORY : 0;
   o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
   o.bad = false;
   o.mod = true;
@@ -573,11 +602,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #else
         (void)src;
         if (pend) {
-          const uint32_t pos = (qt + __popc(pm & ((1u << lane) - 1u))) & (kAdvQ - 1);
+          const uint32_t pos = (qt + __popc(pm & ((1u << lane) - 1u))) % kAdvQ;
           advq[pos] = AdvEntry{r, v.j2, v.j3, v.disc};
         }
         qt += __popc(pm);
-        if (qt - qh >= 32u) {
+        if (qt - qh >= kAdvFlushAt) {
           advisory_flush(a, flags, advq, qh, 32u);
           qh += 32u;
         }
@@ -629,10 +658,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
       for (int k = 0; k < 9; ++k) mm.e[k] = m[k];
       StepOut o;
-      if (__all_sync(0xffffffffu, sym_ok && mod && pmod))
-        o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
-      else
+      if (__all_sync(0xffffffffu, sym_ok && mod && pmod)) {
+#if EIG33_ADV_FUSED && !EIG33_ADVQ_SMEM
+        if (kQueue && qt - qh >= 32u) {
+          __syncwarp();  // queue entries were written by other lanes
+          const AdvEntry e = advq[(qh + lane) % kAdvQ];
+          o = tier_moderate_adv<MODE, WANT_FLAGS>(mm, pc, T.tab, a, flags, e.idx, e.j2, e.j3, e.disc);
+          __syncwarp();
+          qh += 32u;
+        } else
+#endif
+          o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
+      } else {
         o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pbad, T.tab);
+      }
       L = o.L;
       v = o.v;
       f = o.f;
@@ -694,7 +733,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #if EIG33_ADVQ_SMEM
   if (kQueue && qt) advisory_flush_smem(flags, advr, qt);
 #else
-  if (kQueue && qt != qh) advisory_flush(a, flags, advq, qh, qt - qh);  // < 32 left
+  while (kQueue && qt != qh) {  // < kAdvFlushAt left
+    const uint32_t k = qt - qh < 32u ? qt - qh : 32u;
+    advisory_flush(a, flags, advq, qh, k);
+    qh += k;
+  }
 #endif
   tl_mark(3);
 }

@@ -73,13 +73,8 @@ struct AdvEntry {
   long long idx;
   double j2, j3, disc;
 };
-#ifndef EIG33_ADV_FUSED
-#define EIG33_ADV_FUSED 0
-#endif
-// entries per warp: >= 2 x 32 (flush at 32); with EIG33_ADV_FUSED the moderate
-// tier consumes 32 whenever it can and the separate flush waits for 64
-constexpr uint32_t kAdvQ = EIG33_ADV_FUSED ? 96 : 64;
-constexpr uint32_t kAdvFlushAt = EIG33_ADV_FUSED ? 64 : 32;
+constexpr uint32_t kAdvQ = 64;        // entries per warp: >= 2 x 32
+constexpr uint32_t kAdvFlushAt = 32;  // a flush evaluates 32, one per lane
 
 // Evaluate `count` (<= 32) queued records starting at `head`, one per lane,
 // and write their final flag bytes.  Out of line: its registers never enter
@@ -290,29 +285,6 @@ __device__ __forceinline__ StepOut tier_moderate(M9 mm, Carry pc, const double* 
   StepOut o;
   o.L = eig_moderate_bl(pc, tab);
   o.v = invariants_moderate(mm.e);
-  o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
-  o.bad = false;
-  o.mod = true;
-  return o;
-}
-
-// EIG33_ADV_FUSED=1 (measurement variant): when the advisory queue holds >= 32
-// records and the step takes the moderate tier, the 32 advisories are evaluated
-// inside the tier's basic block (one queued record per lane, its 72 B read from
-// L2 at the top), so their dependent chains interleave with the step's DAG
-// instead of running as a separate latency-bound flush.
-template <int MODE, bool WANT_FLAGS>
-__device__ __forceinline__ StepOut tier_moderate_adv(M9 mm, Carry pc, const double* tab,
-                                                     const double* __restrict__ a, uint8_t* __restrict__ flags,
-                                                     long long qidx, double qj2, double qj3, double qdisc) {
-  double qm[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) qm[k] = __ldg(a + qidx * 9 + k);
-  StepOut o;
-  o.L = eig_moderate_bl(pc, tab);
-  o.v = invariants_moderate(mm.e);
-  const bool adv = advisory(qm, Inv{0.0, qj2, qj3, qdisc});
-  flags[qidx] = adv ? EIG33_FLAG_ADVISORY : 0;
   o.f = (MODE == kEig && WANT_FLAGS && o.v.disc < 0.0) ? kPending : 0;
   o.bad = false;
   o.mod = true;
@@ -658,20 +630,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
       for (int k = 0; k < 9; ++k) mm.e[k] = m[k];
       StepOut o;
-      if (__all_sync(0xffffffffu, sym_ok && mod && pmod)) {
-#if EIG33_ADV_FUSED && !EIG33_ADVQ_SMEM
-        if (kQueue && qt - qh >= 32u) {
-          __syncwarp();  // queue entries were written by other lanes
-          const AdvEntry e = advq[(qh + lane) % kAdvQ];
-          o = tier_moderate_adv<MODE, WANT_FLAGS>(mm, pc, T.tab, a, flags, e.idx, e.j2, e.j3, e.disc);
-          __syncwarp();
-          qh += 32u;
-        } else
-#endif
-          o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
-      } else {
+      if (__all_sync(0xffffffffu, sym_ok && mod && pmod))
+        o = tier_moderate<MODE, WANT_FLAGS>(mm, pc, T.tab);
+      else
         o = tier_general<MODE, WANT_FLAGS>(mm, sym_ok, mod, pc, pbad, T.tab);
-      }
       L = o.L;
       v = o.v;
       f = o.f;

@@ -4,12 +4,11 @@ The path shards with no exchange step: every record is independent,
 so a batch is cut into contiguous shards and each GPU (one process per GPU, or
 one host thread per GPU in eig33_multi_eigvals) evaluates its own shard.
 
-* shard_bounds: strong sharding of one given batch -- the formula the C++ host
-  driver uses (paper_2511_00292_b200/csrc/eig33_host.cpp eig33_multi_eigvals):
-  lo_g = 2*floor(g*n/(2G)), even so every shard's device copy stays 16-B
-  aligned for the TMA loads; the last shard takes the remainder.
-* weak_range: bench.py's weak scaling -- rank r owns records
-  [r*n_per_rank, (r+1)*n_per_rank) of one global counter-based corpus.
+shard_bounds: strong sharding of one given batch -- the formula the C++ host
+driver uses (paper_2511_00292_b200/csrc/eig33_host.cpp eig33_multi_eigvals)
+and bench.py's N-rank job: lo_g = 2*floor(g*n/(2G)), even so every shard's
+device copy stays 16-B aligned for the TMA loads; the last shard takes the
+remainder.
 """
 
 
@@ -19,7 +18,3 @@ def shard_bounds(n: int, world: int, rank: int):
     lo = 2 * (rank * n // (2 * world))
     hi = n if rank + 1 == world else 2 * ((rank + 1) * n // (2 * world))
     return lo, hi
-
-
-def weak_range(n_per_rank: int, rank: int):
-    return rank * n_per_rank, (rank + 1) * n_per_rank

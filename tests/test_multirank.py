@@ -11,7 +11,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2511_00292_b200.shard import shard_bounds, weak_range
+from paper_2511_00292_b200.shard import shard_bounds
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 7, 1000, 1001, 2 ** 20 + 3])
@@ -24,9 +24,11 @@ def test_shard_bounds_partition(n, world):
     assert all(lo % 2 == 0 for lo, _ in bounds)
 
 
-def test_weak_ranges_disjoint():
-    r = [weak_range(1 << 28, k) for k in range(8)]
-    assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+def test_strong_shards_of_the_bench_job():
+    """bench.py's N-rank job: 2^28 records cut like eig33_multi_eigvals cuts a batch."""
+    for world in (1, 2, 4, 8):
+        b = [shard_bounds(1 << 28, world, r) for r in range(world)]
+        assert [hi - lo for lo, hi in b] == [(1 << 28) // world] * world
 
 
 def _free_port():

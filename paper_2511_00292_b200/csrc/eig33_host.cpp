@@ -85,8 +85,10 @@ int ensure(Staging& s, size_t cap) {
     if ((e = cudaMalloc(&s.a[i], cap * 9 * sizeof(double))) != cudaSuccess ||
         (e = cudaMalloc(&s.inv[i], cap * 4 * sizeof(double))) != cudaSuccess ||
         (e = cudaMalloc(&s.lam[i], cap * 3 * sizeof(double))) != cudaSuccess ||
-        (e = cudaMalloc(&s.flags[i], cap)) != cudaSuccess)
-      return fail(EIG33_ECUDA, "cudaMalloc staging", e);
+        (e = cudaMalloc(&s.flags[i], cap)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(EIG33_ECUDA, "cudaMalloc staging", e);  // cap stays 0: the next call reallocates
+    }
   }
   s.cap = cap;
   return EIG33_OK;
@@ -258,12 +260,14 @@ int ensure_host(HostStaging& h, size_t cap) {
   }
   h.cap = 0;
   for (int i = 0; i < kSets; ++i) {
-    void *a, *b, *c, *d;
+    void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr;
     if ((e = cudaHostAlloc(&a, cap * 9 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess ||
         (e = cudaHostAlloc(&b, cap * 4 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess ||
         (e = cudaHostAlloc(&c, cap * 3 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess ||
-        (e = cudaHostAlloc(&d, cap, cudaHostAllocPortable)) != cudaSuccess)
+        (e = cudaHostAlloc(&d, cap, cudaHostAllocPortable)) != cudaSuccess) {
+      for (void* p : {a, b, c, d}) cudaFreeHost(p);  // (the sets before i stay; cap stays 0)
       return fail(EIG33_ECUDA, "cudaHostAlloc staging", e);
+    }
     h.in[i] = static_cast<double*>(a);
     h.inv[i] = static_cast<double*>(b);
     h.lam[i] = static_cast<double*>(c);

@@ -521,6 +521,27 @@ def power_model(P, clocks, pa, pl, n, st, stream, dev, torch):
             "model_records_per_s": (cap - p_idle) / e_total}
 
 
+def bind_to_gpu_cpus(local_rank):
+    """At N > 1: pin this rank's process to the CPUs NVML reports as local to
+    its GPU (on a two-socket box, the GPU's own NUMA node), so the pinned host
+    buffers of the e2e leg are allocated and copied on the socket whose PCIe root
+    the GPU hangs off.  Returns the CPU count bound to, or None (NVML
+    unavailable, single NUMA node: nothing changes)."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus and len(cpus) < len(os.sched_getaffinity(0)):
+            os.sched_setaffinity(0, cpus)
+        return len(cpus) or None
+    except Exception:  # noqa: BLE001 -- a binding hint, never a failure
+        return None
+
+
 # ---------------------------------------------------------------------------
 class HostSync:
     """Rank plumbing shared by the GPU arm and the dry run: the default process
@@ -580,6 +601,7 @@ def run_ours(args, rank, world, local_rank):
         raise SystemExit("--warmup must be >= 3")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    bound_cpus = bind_to_gpu_cpus(local_rank) if world > 1 else None
     sync = HostSync(world, "nccl", dev)
     barrier, gather, gather_int = sync.barrier, sync.gather, sync.gather_obj
 
@@ -681,6 +703,7 @@ def run_ours(args, rank, world, local_rank):
                "api": "eig33_eigvals_host per rank on its shard (pinned host buffers, chunked "
                       "H2D/kernel/D2H over 3 streams); wall clock, max over ranks",
                "bitwise_equal_to_device_path": same_all,
+               "rank_cpu_binding": bound_cpus,
                "pcie_roofline": {"bound": "pcie", "h2d_gbs_measured": link["h2d_gbs"],
                                  "d2h_gbs_measured": link["d2h_gbs"],
                                  "concurrent_h2d_gbs": link["h2d_concurrent_gbs"],

@@ -4,7 +4,7 @@
 for v in "" "$@"; do
   so=""; [ -n "$v" ] && so=$PWD/paper_2511_00292_b200/build/variants/$v.so
   printf "%-12s " "${v:-product}"
-  EIG33_SO=$so timeout 300 python bench.py --steps 100 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | python -c "
+  EIG33_SO=$so timeout 300 python bench.py --steps 100 --warmup 3 --no-e2e --no-cpu-baseline --no-per-config --no-multi-driver 2>&1 | python -c "
 import json,sys
 l=sys.stdin.read().strip().splitlines()
 try:

@@ -79,7 +79,7 @@ constexpr uint32_t kAdvFlushAt = 32;  // a flush evaluates 32, one per lane
 // Evaluate `count` (<= 32) queued records starting at `head`, one per lane,
 // and write their final flag bytes.  Out of line: its registers never enter
 // the steady-state loop's allocation.
-__device__ __noinline__ void advisory_flush(const double* __restrict__ a, uint8_t* __restrict__ flags,
+static __device__ __noinline__ void advisory_flush(const double* __restrict__ a, uint8_t* __restrict__ flags,
                                             const AdvEntry* q, uint32_t head, uint32_t count) {
   __syncwarp();  // queue entries were written by other lanes
   const uint32_t lane = threadIdx.x & 31u;
@@ -108,7 +108,7 @@ struct AdvRec {
   long long idx;
 };
 constexpr uint32_t kAdvR = 32;
-__device__ __noinline__ void advisory_flush_smem(uint8_t* __restrict__ flags, const AdvRec* q,
+static __device__ __noinline__ void advisory_flush_smem(uint8_t* __restrict__ flags, const AdvRec* q,
                                                  uint32_t count) {
   __syncwarp();
   const uint32_t lane = threadIdx.x & 31u;
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_triple_angle(const double* __restrict__ j3,
+static __global__ void __launch_bounds__(kThreads) k_triple_angle(const double* __restrict__ j3,
                                                            const double* __restrict__ disc,
                                                            long long n, double* __restrict__ phi) {
   __shared__ __align__(16) double tab[kTabDoubles + 7];

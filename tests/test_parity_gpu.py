@@ -454,12 +454,25 @@ def test_variant_invariants_host_entry_equals_device():
             assert U.bit_equal(eig.invariants(a, variant=v), eig.invariants(d, variant=v).cpu().numpy()).all()
 
 
-def test_study_variants_on_device():
+@pytest.mark.parametrize("n,offset", [((1 << 18), 0), (4099, 0), (1, 0), (70001, 1)])
+def test_study_variants_on_device(n, offset):
     """naive / tensor invariants, eigvals_naive (+advisory), Jacobians vs the
-    compiled reference: bit-exact except eigvals_naive's lambda (tolerance)."""
-    a = U.mixed_corpus(1 << 18, 31)
-    n = a.shape[0]
+    compiled reference: bit-exact except eigvals_naive's lambda (tolerance).
+    The study kernels run on the hot path's TMA ring and chunk scheduler; a
+    ragged size and a record base that is only 8-B aligned (offset 1: the
+    cooperative-load path) are covered too."""
+    base = U.mixed_corpus(n + 1, 31 + n)
+    a = base[offset:offset + n]
     R = U.ref()
+    if offset:  # device input at an 8-B aligned (not 16-B aligned) address
+        buf = torch.from_numpy(np.ascontiguousarray(base).reshape(-1)).cuda()
+        a_dev = buf[9 * offset: 9 * (offset + n)].view(n, 9)
+        assert a_dev.data_ptr() % 16 != 0
+        inv_d = eig.invariants(a_dev, variant="Naive").cpu().numpy()
+        want = np.empty((n, 4))
+        R.ref_invariants_variant(U.ptr(np.ascontiguousarray(a)), U.S(n), 1, U.ptr(want), U.nthreads())
+        assert U.bit_equal(inv_d, want).all()
+    a = np.ascontiguousarray(a)
     for name, v in (("Naive", 1), ("NaiveTensor", 2)):
         got = eig.invariants(a, variant=name)
         want = np.empty((n, 4))

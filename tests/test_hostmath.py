@@ -287,3 +287,21 @@ def test_atan2_any_equals_atan2_pos():
     H.hm_atan2_any(U.ptr(y), U.ptr(x), U.S(n), U.ptr(got))
     H.hm_atan2(U.ptr(y), U.ptr(x), U.S(n), U.ptr(want))
     assert U.bit_equal(got, want).all()
+
+
+def test_tiny_constant_division_is_ieee():
+    """The constant divisions' tiny-operand form (x scaled by 2^120, the two-op
+    quotient, rounding to the subnormal grid with the exact-midpoint repair;
+    eig33_math.cuh div_tiny_fix) equals IEEE x/c for c = 3, 6, 27 on every
+    binade below 2^-963, subnormals, and short mantissas (exact ties for c = 6)."""
+    rng = np.random.default_rng(5)
+    n = 1 << 20
+    x = rng.integers(1, 60 << 52, size=n, dtype=np.int64).view(np.float64) * np.where(rng.random(n) < 0.5, -1, 1)
+    y = np.ldexp(rng.integers(0, 1 << 20, size=n).astype(np.float64), rng.integers(-1074, -990, size=n))
+    z = np.concatenate([x, y, -y, [0.0, -0.0, 5e-324, -5e-324, 3 * 5e-324, 6 * 5e-324, 9 * 5e-324,
+                                   27 * 5e-324, 2.2250738585072014e-308, 2.0 ** -963, -(2.0 ** -963)]])
+    for c in (3, 6, 27):
+        out = np.empty_like(z)
+        U.hostmath().hm_div(U.ptr(z), U.S(z.size), c, U.ptr(out))
+        bad = ~U.bit_equal(out, z / c)
+        assert not bad.any(), (c, z[bad][:5])

@@ -428,6 +428,7 @@ __device__ __forceinline__ void sched_init(Smem& S) {
 #ifndef EIG33_LAZY2
 #define EIG33_LAZY2 1
 #endif
+
 template <bool TMA>
 __device__ __forceinline__ void ring_issue(const WarpRing& R, int s) {
   const long long c = s ? R.cid1 : R.cid0;

@@ -543,13 +543,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
   double m[9];
   bool mod, bad, pmod, pbad, pfast, pvalid;
-  Inv v;
+  Inv v{};  // set by every stage1/step before store_stage1 reads it
   Carry pc;
   uint8_t f;
   long long pr;  // record index of the carried stage
   constexpr bool kQueue = MODE == kEig && WANT_FLAGS;
   AdvEntry* advq = kQueue ? reinterpret_cast<AdvEntry*>(smem_raw + sizeof(Smem)) + warp * kAdvQ : nullptr;
+#if EIG33_ADVQ_SMEM
   AdvRec* advr = kQueue ? reinterpret_cast<AdvRec*>(smem_raw + sizeof(Smem)) + warp * kAdvR : nullptr;
+#endif
   uint32_t qh = 0, qt = 0;  // queue head / tail (warp-uniform, monotone counts)
   // src: this lane's record in the ring (EIG33_ADVQ_SMEM copies it into the queue)
   auto store_stage1 = [&](long long r, bool valid, const double* src) {

@@ -88,6 +88,19 @@ void hm_eigvals(const double* a, size_t n, double* lam, uint8_t* adv) {
     if (adv) adv[i] = advisory(a + 9 * i, v) ? 1 : 0;
   }
 }
+// the advisory decision for given invariants (i1 unused): the product's
+// (certified squared comparison, reference-order fallback) and the
+// reference-order one; and the reference-order tolerance itself
+void hm_advisory2(const double* a, const double* inv, size_t n, uint8_t* fast, uint8_t* ref) {
+  for (size_t i = 0; i < n; ++i) {
+    const Inv v{inv[4 * i], inv[4 * i + 1], inv[4 * i + 2], inv[4 * i + 3]};
+    fast[i] = advisory(a + 9 * i, v) ? 1 : 0;
+    ref[i] = advisory_ref_order(a + 9 * i, v) ? 1 : 0;
+  }
+}
+void hm_disc_tolerance(const double* a, const double* inv, size_t n, double* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = disc_tolerance(a + 9 * i, inv[4 * i + 1], inv[4 * i + 2]);
+}
 void hm_atan2(const double* y, const double* x, size_t n, double* out) {
   for (size_t i = 0; i < n; ++i) out[i] = atan2_pos(y[i], x[i], eig33_tab);
 }

@@ -305,3 +305,52 @@ def test_tiny_constant_division_is_ieee():
         U.hostmath().hm_div(U.ptr(z), U.S(z.size), c, U.ptr(out))
         bad = ~U.bit_equal(out, z / c)
         assert not bad.any(), (c, z[bad][:5])
+
+
+def _advisory2(a, inv):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    inv = np.ascontiguousarray(inv, dtype=np.float64)
+    n = a.shape[0]
+    fast, ref = np.empty(n, np.uint8), np.empty(n, np.uint8)
+    U.hostmath().hm_advisory2(U.ptr(a), U.ptr(inv), U.S(n), U.ptr(fast), U.ptr(ref))
+    return fast, ref
+
+
+def test_advisory_certified_decision_equals_reference_order():
+    """advisory() decides x = -disc vs the tolerance T by a squared comparison
+    without the two square roots (eig33_math.cuh) and falls back to the
+    reference-order T only near a tie: same flag as the reference-order form
+    on the advisory-heavy configs, adversarial inputs, and on synthetic
+    invariants placed within a few ulps of the tie (disc = -T (1 + k 2^-52))."""
+    parts = [U.host_corpus(4, 1 << 17, 104), U.host_corpus(5, 1 << 17, 105),
+             U.host_corpus(5, 1 << 15, 105, first=3 << 20), _adversarial(1 << 14, 91)]
+    a = np.concatenate(parts)
+    inv = U.checker_invariants(a)
+    fast, ref = _advisory2(a, inv)
+    assert (fast == ref).all(), np.nonzero(fast != ref)[0][:5]
+    _, adv_r = U.checker_eigvals(a)
+    assert (fast == adv_r).all()
+    assert fast.sum() > 1000  # the flag-set branch is exercised
+    # near-tie invariants on the records with a finite, normal tolerance
+    n = a.shape[0]
+    T = np.empty(n)
+    U.hostmath().hm_disc_tolerance(U.ptr(a), U.ptr(inv), U.S(n), U.ptr(T))
+    ok = np.isfinite(T) & (T > 1e-290) & (T < 1e290)
+    at, it, Tt = a[ok][:20000], inv[ok][:20000], T[ok][:20000]
+    for k in (-3, -1, 0, 1, 3, 1 << 6, 1 << 9, 1 << 12):
+        it2 = it.copy()
+        it2[:, 3] = -(Tt * (1.0 + k * 2.0 ** -52))
+        f2, r2 = _advisory2(at, it2)
+        assert (f2 == r2).all(), (k, np.nonzero(f2 != r2)[0][:5])
+        if k == 0:
+            assert not r2.any()  # disc == -T is not flagged
+        if k >= 1:
+            assert r2.all()
+    # neighbours of the tie in ulp steps of disc itself
+    for s in (-2, -1, 1, 2):
+        it2 = it.copy()
+        it2[:, 3] = -np.nextafter(Tt, np.inf if s > 0 else 0.0)
+        if abs(s) == 2:
+            it2[:, 3] = -np.nextafter(-it2[:, 3], np.inf if s > 0 else 0.0)
+        f2, r2 = _advisory2(at, it2)
+        assert (f2 == r2).all()

@@ -69,6 +69,18 @@ struct __align__(16) Smem {
 // from HBM, cost 72 us next to k_fused's 121 us on config 4.  Flushing 64 at a
 // time, two records per lane from a 96-entry queue, measured slower: 23.3 vs
 // 24.7 G records/s on config 4.)
+// EIG33_FLUSH_PROBE (measurement builds only): 1 = never flush (pending flag
+// bytes stay unwritten), 2 = flush loads the records but skips the arithmetic.
+// On config 4 with invariants and flags (tools/store_mix.py, 2^22 records):
+// lambda alone 24.5 ps/record, + pushes and stores without any flush 26.3,
+// + the flush's loads and flag stores 29.0, + the arithmetic 31.8.  Staging
+// the records into SMEM ahead of the flush with cp.async (one step early, so
+// the L2 round trip is off the flushing warp's path) measured slower: 29.6 vs
+// 31.0 G records/s on config 4, and -1.8% on config 3 with invariants (the
+// 225-KB SMEM carve-out leaves L1 almost nothing); not adopted.
+#ifndef EIG33_FLUSH_PROBE
+#define EIG33_FLUSH_PROBE 0
+#endif
 struct AdvEntry {
   long long idx;
   double j2, j3, disc;
@@ -89,7 +101,11 @@ static __device__ __noinline__ void advisory_flush(const double* __restrict__ a,
     double m[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) m[k] = __ldg(a + e.idx * 9 + k);
+#if EIG33_FLUSH_PROBE == 2  // measurement: loads only
+    flags[e.idx] = (m[0] + m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7] + m[8] + e.disc) < 0.0;
+#else
     flags[e.idx] = advisory(m, Inv{0.0, e.j2, e.j3, e.disc}) ? EIG33_FLAG_ADVISORY : 0;
+#endif
   }
   __syncwarp();  // the slots may be refilled by the next push
 }
@@ -581,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
           advq[pos] = AdvEntry{r, v.j2, v.j3, v.disc};
         }
         qt += __popc(pm);
-        if (qt - qh >= kAdvFlushAt) {
+        if (EIG33_FLUSH_PROBE != 1 && qt - qh >= kAdvFlushAt) {
           advisory_flush(a, flags, advq, qh, 32u);
           qh += 32u;
         }
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #if EIG33_ADVQ_SMEM
   if (kQueue && qt) advisory_flush_smem(flags, advr, qt);
 #else
-  while (kQueue && qt != qh) {  // < kAdvFlushAt left
+  while (kQueue && EIG33_FLUSH_PROBE != 1 && qt != qh) {  // < kAdvFlushAt left
     const uint32_t k = qt - qh < 32u ? qt - qh : 32u;
     advisory_flush(a, flags, advq, qh, k);
     qh += k;

@@ -1,6 +1,7 @@
-"""Config-3 throughput by output mix (lam / lam+inv / lam+inv+flags / inv only),
-burst timing (20 launches of 2^26 records after 3 warm-ups).  Run against a
-variant with EIG33_SO=... to compare builds."""
+"""Throughput by output mix (lam / lam+inv / lam+inv+flags / inv only), burst
+timing (20 launches after 3 warm-ups); config 3 at 2^26 records by default
+(SM_CONFIG=c, SM_LOG2N=k select another).  Run against a variant with
+EIG33_SO=... to compare builds."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch  # noqa: E402
@@ -8,8 +9,9 @@ import paper_2511_00292_b200 as eig  # noqa: E402
 
 L = eig.lib()
 P = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())
-n = 1 << 26
-a = eig.generate(3, n, seed=103)
+cfg = int(os.environ.get("SM_CONFIG", "3"))
+n = 1 << int(os.environ.get("SM_LOG2N", "26"))
+a = eig.generate(cfg, n, seed=100 + cfg)
 lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
 inv = torch.empty((n, 4), dtype=torch.float64, device="cuda")
 fl = torch.empty((n,), dtype=torch.uint8, device="cuda")
@@ -38,4 +40,4 @@ for name, fn, b in [
     ("inv", lambda: L.eig33cu_invariants(P(a), n, P(inv), st), 104),
 ]:
     t = timeit(fn)
-    print(f"{tag:10s} {name:14s} {n / t / 1e9:6.2f} G rec/s  {n * b / t / 1e12:5.2f} TB/s")
+    print(f"{tag:10s} c{cfg} {name:14s} {n / t / 1e9:6.2f} G rec/s  {n * b / t / 1e12:5.2f} TB/s")

@@ -28,7 +28,12 @@ def rate(fn, n, reps=20):
     return n / (e0.elapsed_time(e1) / reps * 1e-3) / 1e9
 
 
+ONLY = [c for c in os.environ.get("VC_CASES", "").split(",") if c]  # e.g. VC_CASES=c4,c5_q0
+
+
 def case(cfg, n, first=0, name=None):
+    if ONLY and (name or f"c{cfg}") not in ONLY:
+        return
     a = eig.generate(cfg, n, seed=100 + cfg, first_index=first)
     lam = torch.empty((n, 3), dtype=torch.float64, device="cuda")
     inv = torch.empty((n, 4), dtype=torch.float64, device="cuda")

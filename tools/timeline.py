@@ -26,6 +26,8 @@ for lg in (18, 20, 22):
     tl = np.zeros((W, 4), np.uint64)
     assert L.eig33_debug_timeline(tl.ctypes.data, W) == 0
     nw = min(W, (n + 63) // 64)
+    if os.environ.get("TL_SAVE"):
+        np.save(os.path.join(os.environ["TL_SAVE"], f"timeline_2p{lg}.npy"), tl[:nw])
     t = tl[:nw].astype(np.int64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3  # us

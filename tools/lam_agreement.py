@@ -9,7 +9,7 @@ Every config at its BASELINE batch; config 3 at its full 2^28 in 2^25 slices
 (generated on the device slice by slice, counter-based, so memory stays
 bounded).  The worst records (strict reading) are saved for analysis.
 
-  python tools/lam_agreement.py [--out DIR] [--configs 1,2,3,4,5] [--full3]
+  python tools/lam_agreement.py [--out DIR] [--configs 1,2,3,4,5] [--seed-base 1000]
 """
 import argparse
 import os

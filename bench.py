@@ -47,6 +47,7 @@ N_TOTAL_DEFAULT = 1 << 28
 SEED = 0x2511_00292
 BYTES_PER_REC = 96          # 72 B in + 24 B lambda out
 BYTES_PER_REC_FULL = 129    # + 32 B invariants + 1 B flags
+BYTES_PER_REC_INV = 104     # invariants alone: 72 B in + 32 B out
 FP64_OPS_PER_REC = 357      # frozen algorithmic FP64-pipe count
 HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 SPEC_FP64_INST_PER_S = 148 * 64 * 1.965e9  # 148 SMs x 64 FP64 lanes x max SM clock
@@ -375,18 +376,19 @@ def ncu_traffic():
         return None, None
 
 
-def roofline(rate_per_gpu, bytes_per_rec, hbm_peak, hbm_src, fp64_peak, fp64_src):
+def roofline(rate_per_gpu, bytes_per_rec, hbm_peak, hbm_src, fp64_peak, fp64_src, ops=FP64_OPS_PER_REC):
     """Both roofs for one kernel at `rate_per_gpu` records/s; the binding roof
-    (the slower one for this record mix) on top."""
+    (the slower one for this record mix) on top.  `ops` = algorithmic FP64
+    instructions per record (0: an HBM-only kernel, the invariants alone)."""
     hbm_ach = rate_per_gpu * bytes_per_rec / 1e9
-    fp64_ach = rate_per_gpu * FP64_OPS_PER_REC / 1e12
+    fp64_ach = rate_per_gpu * ops / 1e12
     hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
            "peak_source": hbm_src, "bytes_per_record": bytes_per_rec}
     fp64 = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "T fp64-inst/s",
             "frac": fp64_ach / fp64_peak if fp64_peak else None, "peak_source": fp64_src,
             "frac_of_spec": fp64_ach * 1e12 / SPEC_FP64_INST_PER_S,
             "spec_peak": SPEC_FP64_INST_PER_S / 1e12,
-            "ops_per_record": FP64_OPS_PER_REC}
+            "ops_per_record": ops}
     binding = fp64 if (fp64["frac"] or 0) >= hbm["frac"] else hbm
     out = dict(binding)
     out["both"] = {"hbm": hbm, "fp64": fp64}
@@ -407,8 +409,12 @@ def time_launches(fn, stream, reps, torch):
 def per_config_block(L, eig, torch, dev, stream, reps=20):
     """Configs 1-5 at their BASELINE sizes (config 3 at 2^22 here; its 2^28 is
     the headline): lambda only (96 B/record) and lambda + invariants + flags
-    (129 B/record, what configs 1, 4 and 5 ask for).  Burst rates: 20
-    launches each after 3 warm-ups, on a GPU that idled 0.5 s first."""
+    (129 B/record, what configs 1, 4 and 5 ask for); plus the other batched
+    entry points on the config they fit: eigvalss with invariants and flags on
+    the symmetric config 1 (src/eigensolver.cpp:97-117, 129 B/record) and the
+    invariants alone on config 3 (src/invariants.cpp:76-98, 104 B/record,
+    HBM-bound).  Burst rates: 20 launches each after 3 warm-ups, on a GPU that
+    idled 0.5 s first."""
     out = {}
     for cfg, n in CONFIG_SIZES.items():
         with torch.cuda.stream(stream):
@@ -420,10 +426,16 @@ def per_config_block(L, eig, torch, dev, stream, reps=20):
         pa, pl, pi, pf = (ctypes.c_void_p(x.data_ptr()) for x in (a, lam, inv, fl))
         st = ctypes.c_void_p(stream.cuda_stream)
         row = {"records": n}
-        for mode, args_, bpr in (("lam", (None, pl, None), BYTES_PER_REC),
-                                 ("lam_inv_flags", (pi, pl, pf), BYTES_PER_REC_FULL)):
-            def fn(args_=args_):
-                rc = L.eig33cu_eigvals(pa, n, *args_, st)
+        modes = [("lam", L.eig33cu_eigvals, (None, pl, None), BYTES_PER_REC, FP64_OPS_PER_REC),
+                 ("lam_inv_flags", L.eig33cu_eigvals, (pi, pl, pf), BYTES_PER_REC_FULL, FP64_OPS_PER_REC)]
+        if cfg == 1:
+            modes.append(("eigvalss_inv_flags", L.eig33cu_eigvalss, (pi, pl, pf), BYTES_PER_REC_FULL,
+                          FP64_OPS_PER_REC))
+        if cfg == 3:
+            modes.append(("inv_only", L.eig33cu_invariants, (pi,), BYTES_PER_REC_INV, 0))
+        for mode, entry, args_, bpr, ops in modes:
+            def fn(entry=entry, args_=args_):
+                rc = entry(pa, n, *args_, st)
                 if rc:
                     raise RuntimeError(L.eig33cu_last_error().decode())
             time.sleep(0.5)
@@ -433,7 +445,7 @@ def per_config_block(L, eig, torch, dev, stream, reps=20):
             rate = n / (ms * 1e-3)
             row[mode] = {"value": rate, "unit": UNIT, "ms_per_launch": ms, "launches": reps,
                          "kernels_per_launch": 1,
-                         "roofline": {"bytes_per_record": bpr}}  # fractions filled in after the FP64 probe
+                         "roofline": {"bytes_per_record": bpr, "ops_per_record": ops}}  # fractions: after the FP64 probe
         if cfg == 4 or cfg == 5:
             adv = int((fl.to(torch.int32) & 1).sum().item())
             row["advisory_share"] = adv / n
@@ -784,9 +796,9 @@ def run_ours(args, rank, world, local_rank):
         fp64_sus = P.eig33_probe_fp64_chaos(2.5)
     if per_config:
         for row in per_config.values():
-            for mode in ("lam", "lam_inv_flags"):
+            for mode in [k for k, v in row.items() if isinstance(v, dict) and "roofline" in v]:
                 rf = roofline(row[mode]["value"], row[mode]["roofline"]["bytes_per_record"], hbm_peak, hbm_src,
-                              fp64_burst / 1e12, fp64_src_b)
+                              fp64_burst / 1e12, fp64_src_b, ops=row[mode]["roofline"]["ops_per_record"])
                 row[mode]["roofline"].update(bound=rf["bound"], frac=rf["frac"], frac_hbm=rf["both"]["hbm"]["frac"],
                                              frac_fp64=rf["both"]["fp64"]["frac"])
 

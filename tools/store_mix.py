@@ -38,6 +38,8 @@ for name, fn, b in [
     ("lam+inv", lambda: L.eig33cu_eigvals(P(a), n, P(inv), P(lam), None, st), 128),
     ("lam+inv+flags", lambda: L.eig33cu_eigvals(P(a), n, P(inv), P(lam), P(fl), st), 129),
     ("inv", lambda: L.eig33cu_invariants(P(a), n, P(inv), st), 104),
+    ("sym lam", lambda: L.eig33cu_eigvalss(P(a), n, None, P(lam), None, st), 96),
+    ("sym lam+inv+fl", lambda: L.eig33cu_eigvalss(P(a), n, P(inv), P(lam), P(fl), st), 129),
 ]:
     t = timeit(fn)
     print(f"{tag:10s} c{cfg} {name:14s} {n / t / 1e9:6.2f} G rec/s  {n * b / t / 1e12:5.2f} TB/s")

@@ -428,7 +428,8 @@ def per_config_block(L, eig, torch, dev, stream, reps=20):
         row = {"records": n}
         modes = [("lam", L.eig33cu_eigvals, (None, pl, None), BYTES_PER_REC, FP64_OPS_PER_REC),
                  ("lam_inv_flags", L.eig33cu_eigvals, (pi, pl, pf), BYTES_PER_REC_FULL, FP64_OPS_PER_REC)]
-        if cfg == 1:
+        if cfg == 1:  # symmetric: the reference's own entry point for it is eigvalss
+            modes.append(("eigvalss_lam", L.eig33cu_eigvalss, (None, pl, None), BYTES_PER_REC, FP64_OPS_PER_REC))
             modes.append(("eigvalss_inv_flags", L.eig33cu_eigvalss, (pi, pl, pf), BYTES_PER_REC_FULL,
                           FP64_OPS_PER_REC))
         if cfg == 3:

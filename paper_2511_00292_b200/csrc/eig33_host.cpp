@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <initializer_list>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -128,8 +129,8 @@ bool is_pinned(const void* p) {
 }
 
 // Parallel memcpy for the staged (pageable-buffer) pipeline: a persistent pool
-// of host threads splits each copy into 4 MB parts; the calling thread works on
-// its own copy too.  Several copies may be in flight at once (the multi-GPU
+// of host threads splits each copy into 1 MB parts; the calling thread works on
+// its own copies too (copy_all: a chunk's outputs and the next input at once).  Several copies may be in flight at once (the multi-GPU
 // driver runs one host thread per device): each copy is a Job with its own
 // counters, idle workers join any job that still has unclaimed parts, and a
 // copy returns only after every part is done AND no worker still holds a
@@ -141,31 +142,53 @@ class CopyPool {
     static CopyPool* p = new CopyPool;
     return *p;
   }
-  void copy(void* dst, const void* src, size_t bytes) {
-    if (bytes < 2 * kPart || nworkers_ == 0) {
-      std::memcpy(dst, src, bytes);
-      return;
+  struct Span {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  void copy(void* dst, const void* src, size_t bytes) { copy_all({Span{dst, src, bytes}}); }
+  // Several copies at once (e.g. one chunk's input and an older chunk's
+  // outputs): all their parts go to the pool together, the caller works too,
+  // and the call returns when every one is complete.
+  void copy_all(std::initializer_list<Span> spans) {
+    Job jobs[4];
+    size_t nj = 0;
+    for (const Span& sp : spans) {
+      if (sp.bytes == 0) continue;
+      if (sp.bytes < 2 * kPart || nworkers_ == 0 || nj == 4) {
+        std::memcpy(sp.dst, sp.src, sp.bytes);
+        continue;
+      }
+      Job& j = jobs[nj++];
+      j.dst = static_cast<char*>(sp.dst);
+      j.src = static_cast<const char*>(sp.src);
+      j.bytes = sp.bytes;
+      j.nparts = (sp.bytes + kPart - 1) / kPart;
     }
-    Job j;
-    j.dst = static_cast<char*>(dst);
-    j.src = static_cast<const char*>(src);
-    j.bytes = bytes;
-    j.nparts = (bytes + kPart - 1) / kPart;
+    if (nj == 0) return;
     {
       std::lock_guard<std::mutex> g(mu_);
-      jobs_.push_back(&j);
+      for (size_t k = 0; k < nj; ++k) jobs_.push_back(&jobs[k]);
     }
     cv_.notify_all();
-    run(j);
+    for (size_t k = 0; k < nj; ++k) run(jobs[k]);
     std::unique_lock<std::mutex> g(mu_);
-    done_cv_.wait(g, [&] { return j.done.load() == j.nparts && j.refs == 0; });
-    unlink(&j);
+    for (size_t k = 0; k < nj; ++k) {
+      Job& j = jobs[k];
+      done_cv_.wait(g, [&] { return j.done.load() == j.nparts && j.refs == 0; });
+      unlink(&j);
+    }
   }
 
  private:
+// 1 MB parts: a 2^20-record chunk's 24-MB lambda copy then spreads over every
+// worker (4 MB parts left most of 16 idle: +18% on 2^24 pageable records,
+// tools/pageable_rate.py; streaming stores instead of memcpy measured no change)
 #ifndef EIG33_COPY_PART
-#define EIG33_COPY_PART (size_t(4) << 20)
+#define EIG33_COPY_PART (size_t(1) << 20)
 #endif
+
   static constexpr size_t kPart = EIG33_COPY_PART;
   struct Job {
     char* dst = nullptr;
@@ -318,13 +341,17 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
   CopyPool& pool = CopyPool::get();
   const bool out_inv = h_inv != nullptr;
   const size_t nchunks = (n + chunk - 1) / chunk;
-  auto copy_out = [&](size_t c) -> int {
+  // copy-out of chunk c (after its D2H), together with the copy-in of the
+  // chunk that reuses its set (nxt < n), in one pool round
+  auto copy_out = [&](size_t c, size_t nxt) -> int {
     const int b = int(c % kSets);
     const size_t lo = c * chunk, cnt = std::min(chunk, n - lo);
     const cudaError_t e = cudaEventSynchronize(h.done[b]);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "staged D2H", e);
-    if (out_inv) pool.copy(h_inv + lo * 4, h.inv[b], cnt * 4 * sizeof(double));
-    if (!inv_only(op)) pool.copy(h_lam + lo * 3, h.lam[b], cnt * 3 * sizeof(double));
+    const size_t ilo = nxt * chunk, icnt = nxt < nchunks ? std::min(chunk, n - ilo) : 0;
+    pool.copy_all({{out_inv ? h_inv + lo * 4 : nullptr, h.inv[b], out_inv ? cnt * 4 * sizeof(double) : 0},
+                   {inv_only(op) ? nullptr : h_lam + lo * 3, h.lam[b], inv_only(op) ? 0 : cnt * 3 * sizeof(double)},
+                   {h.in[b], icnt ? h_a + ilo * 9 : h_a, icnt * 9 * sizeof(double)}});
     if (want_flags) std::memcpy(flags_out + lo, h.fl[b], cnt);
     return EIG33_OK;
   };
@@ -332,8 +359,11 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
     const int b = int(c % kSets);
     cudaStream_t st = s.st[b];
     const size_t lo = c * chunk, cnt = std::min(chunk, n - lo);
-    if (c >= (size_t)kSets && (rc = copy_out(c - kSets))) return rc;  // also frees set b
-    pool.copy(h.in[b], h_a + lo * 9, cnt * 9 * sizeof(double));
+    if (c >= (size_t)kSets) {  // frees set b and fills its input with chunk c
+      if ((rc = copy_out(c - kSets, c))) return rc;
+    } else {
+      pool.copy(h.in[b], h_a + lo * 9, cnt * 9 * sizeof(double));
+    }
     cudaError_t e = cudaMemcpyAsync(s.a[b], h.in[b], cnt * 9 * sizeof(double), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(EIG33_ECUDA, "H2D", e);
     rc = launch_op(op, s.a[b], cnt, out_inv ? s.inv[b] : nullptr, s.lam[b],
@@ -351,7 +381,7 @@ int run_staged(Op op, Staging& s, const double* h_a, size_t n, double* h_inv, do
     if ((e = cudaEventRecord(h.done[b], st)) != cudaSuccess) return fail(EIG33_ECUDA, "event", e);
   }
   for (size_t c = nchunks > (size_t)kSets ? nchunks - kSets : 0; c < nchunks; ++c)
-    if ((rc = copy_out(c))) return rc;
+    if ((rc = copy_out(c, nchunks))) return rc;
   return EIG33_OK;
 }
 
